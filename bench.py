@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: count the models of a Boolean program over all
+2^n valuations of the free generators (arXiv 1310.6978 §2.3, Prop 2.2).
+
+Default workload (the config BASELINE.json's metric is quoted on: register
+mode count at 1/2/4/8 GPUs against the int-ALU roofline) is config C5: a
+random 1000-gate Boolean DAG over n = 42 variables, 2^42 valuations per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3_posets]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
+    python bench.py --impl reference ...                   (the CPU oracle arm)
+
+A step = one full pass of the hot path over the step's batch: every rank
+counts its cofactor range [r 2^(n-p), (r+1) 2^(n-p)) with the JIT'd
+register-mode kernel (generators synthesised in registers, straight-line
+LOP3 body, fused popcount + block/grid reduction), then ONE NCCL all-reduce
+of the 8-byte count (P > 1).  Timing: W untimed warm-up steps; L2 flushed
+(256 MiB write) before every timed step; CUDA events on the launching stream
+around each step; barrier + synchronize on both sides; max over ranks.
+Prints one JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import workloads as W  # noqa: E402
+
+# guide unit counts (B300_MICROARCH.md "Pipe rates": LOP3 on the alu pipe,
+# rt_SMSP = 2 -> 16 lanes/clk per SM sub-partition, 4 per SM -> 64 LOP3/clk/SM)
+SMS = 148
+LOP3_PER_CLK_PER_SM = 64
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="bfa", choices=["bfa", "reference"])
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+CONFIG_DESC = {
+    "c5": "random 1000-gate Boolean DAG over n=42 vars, count mode (BASELINE configs[4])",
+    "c4": "labeled partial orders on 6 points, n=36, count mode (BASELINE configs[3])",
+    "c3_posets": "labeled partial orders on 5 points, n=25, count mode (BASELINE configs[2])",
+    "c3_equiv": "equivalence relations on 5 points, n=25, count mode (BASELINE configs[2])",
+}
+
+
+def config_block(name, n, info, world):
+    return {"workload": f"{name}: {CONFIG_DESC.get(name, name)}", "n": n,
+            "valuations_per_step": 1 << n, "gates_G": info["gates"] if info else None,
+            "luts_L": info["luts"] if info else None, "support": info["support"] if info else None,
+            "seed": W.SEED, "parallelism": f"cofactor x{world} (top log2(P) variable ids)",
+            "l2": "count mode reads no HBM inputs (generators synthesised in registers); "
+                  "L2 flushed with a 256 MiB write before every timed step anyway"}
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = [r for r in self.rows if len(r) >= 8]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in rows for k in range(4) if r[4 + k] == "Active"})
+        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------- oracle (CPU) leg
+def oracle_rate(text, n, seconds, threads=None):
+    """Time the CPU oracle, as it stands, on a bounded sample of the workload:
+    a contiguous sub-cube of valuations sized for ~`seconds` of CPU work."""
+    import oracle
+    threads = threads or oracle.default_threads()
+    k = 14
+    while True:
+        t0 = time.perf_counter()
+        oracle.count(text, n, 0, 1 << k, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.5 or k >= n:
+            break
+        k += 2
+    rate = (1 << k) / dt
+    k2 = min(n, max(k, int(rate * seconds).bit_length() - 1))
+    lo = (1 << n) - (1 << k2) if n > k2 else 0   # a sub-cube away from mu = 0
+    t0 = time.perf_counter()
+    oracle.count(text, n, lo, lo + (1 << k2), threads=threads)
+    dt = time.perf_counter() - t0
+    return (1 << k2) / dt, threads, f"sub-cube of 2^{k2} valuations [{lo}, {lo + (1 << k2)}), {dt:.1f} s"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    text, n, _ = W.config(args.config)
+    steps = []
+    for i in range(args.warmup + args.steps):
+        v, cores, sample = oracle_rate(text, n, args.cpu_seconds / 3)
+        if i >= args.warmup:
+            steps.append(v)
+    value = statistics.median(steps)
+    line = {"impl": "reference", "metric": "valuations/s", "value": value, "unit": "valuations/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": (1 << n) / value * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bool (C int per valuation)", "data": "synthetic",
+            "config": config_block(args.config, n, None, 1),
+            "cpu_baseline": {"value": value, "unit": "valuations/s", "cores": cores, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def measure_lop3_peak(bfa, torch, dev):
+    """Measured LOP3 issue rate (reported next to the derived peak)."""
+    sink = torch.zeros(4096, dtype=torch.int32, device=dev)
+    blocks, threads, iters = SMS * 8, 256, 2000
+    bfa.peak_lop3(blocks, threads, 10, sink)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    bfa.peak_lop3(blocks, threads, iters, sink)
+    e.record()
+    torch.cuda.synchronize()
+    dt = s.elapsed_time(e) / 1e3
+    return blocks * threads * iters * 256 / dt
+
+
+def run_bfa(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1310_6978_b200 as bfa
+    from paper_1310_6978_b200.dist import rank_range
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    text, n, expect = W.config(args.config)
+    prog = bfa.Program(text)
+    info = prog.info
+    lo, hi = rank_range(n, rank, world)
+    stream = torch.cuda.current_stream()
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        prog.count_range(n, lo, hi, out=cnt, stream=stream)
+        if world > 1:
+            dist.all_reduce(cnt)
+
+    # JIT + warm-up (untimed)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    launch = bfa.last_launch()
+    result = int(cnt.item()) & ((1 << 64) - 1)
+
+    clocks = ClockSampler(local)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                      # L2 flush, outside the events
+        starts[i].record(stream)
+        kstarts[i].record(stream)
+        prog.count_range(n, lo, hi, out=cnt, stream=stream)
+        kends[i].record(stream)
+        if world > 1:
+            dist.all_reduce(cnt)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
+    t_total = sum(step_ms) / 1e3
+    t_kern = sum(kern_ms) / 1e3
+    if world > 1:
+        tt = torch.tensor([t_total, t_kern], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_total, t_kern = tt.tolist()
+    final = int(cnt.item()) & ((1 << 64) - 1)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    valuations = (1 << n) * args.steps
+    value = valuations / t_total
+    words_per_launch = (hi - lo) >> 5
+    L = info["luts"]
+    kernel_s = t_kern / args.steps
+    # Work per 32-bit word of the cover the kernel must execute: the JIT'd
+    # program is the LUT3 cover of f cofactored on the slot variables, with
+    # loop-invariant LUTs hoisted.
+    seg = max(launch["segments"], key=lambda g: g["words"])
+    S, m = seg["words_per_iter"], seg["m"]
+    L_exec = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
+    achieved = L_exec * words_per_launch / kernel_s           # LOP3/s per GPU
+    sm_clock = clk["sm_max_mhz"] or 1965.0
+    peak_derived = SMS * LOP3_PER_CLK_PER_SM * sm_clock * 1e6
+    peak_measured = measure_lop3_peak(bfa, torch, dev)
+
+    # e2e: the public C-ABI call with a host result (bfa_count -> uint64 on the
+    # host: launch + 8-byte D2H + sync every step).  Count mode has no input
+    # buffers: the program is in the JIT'd instruction stream.
+    if world == 1:
+        prog.count(n)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_count = prog.count(n)
+        e2e_value = valuations / (time.perf_counter() - t0)
+        assert e2e_count == final
+    else:
+        e2e_value = None
+        e2e_count = final
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        v, cores, sample = oracle_rate(text, n, args.cpu_seconds)
+        cpu = {"value": v, "unit": "valuations/s", "cores": cores, "kind": "oracle", "sample": sample}
+
+    kernels_per_step = launch.get("kernels", 1)
+    line = {
+        "metric": "valuations/s", "value": value, "unit": "valuations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32 (bitwise LOP3 on 32-valuation words)",
+        "data": "synthetic (seeded generator, workloads/__init__.py)",
+        "config": config_block(args.config, n, info, world),
+        "count": final, "count_expected": expect,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_derived, "unit": "LOP3/s",
+                     "frac": achieved / peak_derived, "traffic": None,
+                     "per_unit": f"{L_exec:.2f} LOP3 per 32-bit word (32 valuations) of the slot-cofactored, "
+                                 f"hoisted cover ({seg['luts_inner']} inner LUTs / {S} words + "
+                                 f"{seg['luts_outer']} outer LUTs / {S << m} words)",
+                     "nominal_L": L, "nominal_frac": L * words_per_launch / kernel_s / peak_derived,
+                     "units_per_launch": words_per_launch,
+                     "peak_source": f"derived: {SMS} SMs x {LOP3_PER_CLK_PER_SM} LOP3/clk/SM x {sm_clock:.0f} MHz "
+                                    "(B300_MICROARCH.md alu-pipe rate; sm_max clock)",
+                     "peak_measured_lop3": peak_measured, "frac_of_measured": achieved / peak_measured,
+                     "gate_word_ops_per_s": info["gates"] * words_per_launch / kernel_s},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
+                "call": "bfa_count(prog, n) -> host uint64"},
+        "gpu_launches": kernels_per_step * args.steps,
+        "kernel_ms_per_step": kernel_s * 1e3,
+        "launch": launch,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_bfa(args)
+
+
+if __name__ == "__main__":
+    main()

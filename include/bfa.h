@@ -1,0 +1,181 @@
+/*
+ * bfa.h -- C ABI of libbfa: evaluate a Boolean term on the free generators
+ * of the free Boolean algebra on B200 (sm_100a).
+ *
+ * The operation (§1 property (P); Prop 2.2):
+ *   Let f(x_0..x_{n-1}) be a Boolean expression.  The free generators
+ *   b_0..b_{n-1} of Omega_n = B^(2^n) are 2^n-bit vectors (rows of the matrix
+ *   M whose columns are the binary expansions of 0..2^n-1).
+ *   d = f(b_0..b_{n-1}), evaluated bitwise, codes the full DNF of f:
+ *       bit mu of d  =  f evaluated at the valuation  x_v = (mu >> v) & 1.
+ *   The number of models of f is the popcount of d.
+ *
+ * Conventions (readings C-1..C-8):
+ *   - variable id v <-> bit v of the valuation index mu (LSB first); the
+ *     paper's b_1 (MSB row) is id n-1.
+ *   - a DNF vector of n variables is ceil(2^n / 64) (at least 1) little-endian
+ *     uint64 words; bit mu lives in word mu >> 6 at bit mu & 63.  For n < 6
+ *     the unused high bits of word 0 are 0.
+ *   - 0 <= n <= 63; every variable id used by the program must be < n;
+ *     unused ids < n are free (each doubles the count).
+ *
+ * Expression grammar (UTF-8 text; the compiler and the CPU oracle implement it
+ * independently):
+ *   program := { stmt (';' | NEWLINE) } [stmt]       '#' comments to end of line
+ *   stmt    := 'let' NAME '=' expr                   shared subterm, not a constraint
+ *            | NAME '=' expr                         constraint; NAME is also bound
+ *            | expr                                  constraint
+ *   expr    := imp { '<->' imp }                     IFF, left-assoc
+ *   imp     := or [ '->' imp ]                       IMP, right-assoc
+ *   or      := xor { '|' xor }
+ *   xor     := and { '^' and }                       XOR is the paper's '+'
+ *   and     := unary { '&' unary }
+ *   unary   := '~' unary | atom
+ *   atom    := 'x'DIGITS (id <= 62) | '0' | '1' | NAME | '(' expr ')'
+ *   Newlines inside parentheses are whitespace.  The program's value is the
+ *   conjunction of all constraint statements (a system e_i = phi_i is solved
+ *   when every phi_i = 1); no constraints -> constant 1.
+ *   A NAME must be bound before use and may be bound once.
+ *
+ * Ownership: bfa_prog is created by bfa_compile and owned by the caller until
+ * bfa_free; it is immutable after compilation (launch options aside) and may be
+ * shared between threads.  It owns its per-device JIT modules.  All output
+ * buffers are caller-owned DEVICE memory on the current CUDA device.  The
+ * library never returns memory to the caller; materialised mode allocates and
+ * frees its own scratch inside the call.
+ *
+ * Errors: functions returning int return BFA_OK (0) or a negative BFA_E_*
+ * code; bfa_count returns UINT64_MAX on error (never a valid count, since
+ * counts are <= 2^63).  bfa_last_error() returns a thread-local message for
+ * the last failing call (valid until the next call on that thread).  Zero
+ * models is not an error.  There is NO CPU fallback: without a CUDA device
+ * every compute call fails with BFA_E_CUDA.
+ */
+#ifndef BFA_H
+#define BFA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BFA_OK        0
+#define BFA_E_PARSE  -1   /* syntax / name error; message carries line:col       */
+#define BFA_E_ARG    -2   /* NULL pointer, misaligned range, bad option          */
+#define BFA_E_RANGE  -3   /* n > 63, n <= max variable id, range outside [0,2^n) */
+#define BFA_E_CUDA   -4   /* CUDA runtime/driver failure or no device            */
+#define BFA_E_JIT    -5   /* NVRTC / module load failure                         */
+#define BFA_E_NOMEM  -6
+
+typedef struct bfa_prog bfa_prog;
+
+typedef struct {
+  int32_t  max_var_id;   /* largest variable id used, -1 if none                      */
+  int32_t  const_value;  /* -1: not constant; 0 / 1: reduced to that constant        */
+  uint64_t tree_nodes;   /* nodes of the binary expression tree as written
+                            (the paper's 2^l; let refs count 1)     */
+  uint32_t gates;        /* G: 2-input gates of the reduced, hash-consed DAG (NOT free) */
+  uint32_t luts;         /* L: LOP3 (3-input LUT) nodes of the unspecialised cover      */
+  uint32_t support;      /* number of distinct variable ids used                       */
+  uint32_t lets;         /* number of let / named bindings                             */
+} bfa_info;
+
+/* ---- compile (host only; "Translate" + "Reduction") ---- */
+
+/* Parse expr, build the hash-consed gate DAG, propagate constants (Reduction)
+ * and compute the LUT3 cover.  On success *out owns a new program. */
+int bfa_compile(const char* expr, bfa_prog** out);
+void bfa_free(bfa_prog* p);                                 /* NULL-safe */
+int bfa_info_get(const bfa_prog* p, bfa_info* out);
+
+/* Launch options (part of the JIT cache key).  Keys:
+ *   "slot_bits"     log2 words per thread per iteration, 0..3   (default 2)
+ *   "thread_bits"   log2 threads per block, 5..10               (default 8)
+ *   "inner_bits"    max log2 inner-loop trip count, 0..8        (default 4)
+ *   "blocks_per_sm" resident blocks per SM targeted, 0 = occupancy API (default 0)
+ *   "force_generic" 1 = always use the unspecialised word-per-thread kernel
+ *   "engine"        0 = JIT straight-line LOP3 (default), 1 = constant-memory
+ *                   interpreter (ablation)
+ * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
+int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
+
+/* ---- register-synthesised mode (generators built in registers) ---- */
+
+/* Number of models of p over all 2^n valuations; synchronous, current device,
+ * legacy default stream.  UINT64_MAX on error. */
+uint64_t bfa_count(const bfa_prog* p, int n);
+
+/* Full-DNF vector of p: out is a device pointer to >= max(1, 2^(n-6)) u64
+ * words; synchronous, current device. */
+int bfa_eval(const bfa_prog* p, int n, uint64_t* out);
+
+/* Models with mu in [mu_lo, mu_hi), written (not accumulated) to the single
+ * device u64 *count_dev, asynchronously on `stream` (a cudaStream_t; NULL =
+ * legacy default stream).  mu_lo and mu_hi must be multiples of 32, or the
+ * range must be the whole [0, 2^n). */
+int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
+                    uint64_t* count_dev, void* stream);
+
+/* The slice [mu_lo, mu_hi) of the DNF vector, asynchronously on `stream`:
+ * bit (mu - mu_lo) at word (mu - mu_lo) >> 6 of out_dev (device,
+ * ceil((mu_hi-mu_lo)/64) words).  mu_lo, mu_hi multiples of 64, or the whole
+ * range.  If count_dev is non-NULL the slice's popcount is fused and written
+ * there. */
+int bfa_eval_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
+                   uint64_t* out_dev, uint64_t* count_dev, void* stream);
+
+/* ---- materialised mode (the paper's vector formulation) ---- */
+
+/* Fill the generator table S: row v (0 <= v < n_rows) is
+ * the 2^n-bit free generator b_v, at table_dev + v * max(1, 2^(n-6)) words. */
+int bfa_fill_generators(int n, int n_rows, uint64_t* table_dev, void* stream);
+
+/* Evaluate p with every generator and intermediate vector materialised in
+ * HBM.  variant 0: vector algebra, one full-vector LOP3 pass per LUT node
+ * (the program list lives in __constant__ memory); variant 1: fused, 128-bit
+ * loads of the generator table and the LOP3 body in registers.  out_dev as in
+ * bfa_eval; count_dev (nullable) receives the popcount.  Synchronous on
+ * `stream`.  Requires n >= 7. */
+int bfa_eval_materialised(const bfa_prog* p, int n, int variant, uint64_t* out_dev,
+                          uint64_t* count_dev, void* stream);
+
+/* Popcount of n_words device u64 words into *count_dev (written). */
+int bfa_popcount(const uint64_t* vec_dev, uint64_t n_words, uint64_t* count_dev, void* stream);
+
+/* ---- measurement ---- */
+
+/* LOP3 throughput microbenchmark: launches blocks x threads threads, each
+ * executing `iters` x 256 dependent-free lop3.b32 (8 independent chains).
+ * The caller times it; ops = blocks * threads * iters * 256. */
+int bfa_peak_lop3(int blocks, int threads, int iters, uint32_t* sink_dev, void* stream);
+
+/* Statistics of the kernel variant the last launch on this thread used:
+ * executed LUTs per 32-bit word at each loop level etc., as a JSON object
+ * written to buf (NUL-terminated, truncated to len). */
+int bfa_last_launch_json(char* buf, size_t len);
+
+/* ---- introspection (host only; usable without a GPU) ---- */
+
+/* what = 0: LUT3 cover IR text, one line per LUT:
+ *           "L<k> = lop3(<a>, <b>, <c>, 0x<imm>)" with operands "x<id>",
+ *           "L<j>" or "0x<word>", followed by "out = [~]<operand>".
+ * what = 1: CUDA source of the specialised count kernel for n.
+ * what = 2: CUDA source of the specialised eval kernel for n.
+ * what = 3: CUDA source of the unspecialised (generic) count kernel.
+ * Returns the full length needed (excluding NUL) or a negative error. */
+int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len);
+
+/* JIT-compile kernel `what` (1..3 as in bfa_dump) for sm_100a without a
+ * device and return the cubin size; if buf is non-NULL copy up to len bytes.
+ * Lets the build check every generated kernel on a CPU-only host. */
+int64_t bfa_jit_cubin(const bfa_prog* p, int what, int n, void* buf, size_t len);
+
+const char* bfa_last_error(void);
+const char* bfa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BFA_H */

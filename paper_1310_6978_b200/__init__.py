@@ -1,0 +1,220 @@
+"""paper_1310_6978_b200 -- B200-native evaluation of Boolean terms on the free
+generators of the free Boolean algebra (arXiv 1310.6978, §2.3).
+
+Thin ctypes binding over the C ABI of libbfa.so (include/bfa.h): argument
+marshalling only; every step of the hot path runs in the library's sm_100a
+kernels.  PyTorch provides device memory and streams.  There is no CPU
+fallback: if libbfa.so is missing, importing the binding's entry points
+raises, and without a CUDA device every compute call raises BfaError.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+__all__ = ["Program", "BfaError", "words_for", "last_launch", "fill_generators", "popcount",
+           "peak_lop3", "lib_path", "version"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libbfa.so")
+_lib = None
+
+BFA_OK, BFA_E_PARSE, BFA_E_ARG, BFA_E_RANGE, BFA_E_CUDA, BFA_E_JIT, BFA_E_NOMEM = 0, -1, -2, -3, -4, -5, -6
+UINT64_MAX = (1 << 64) - 1
+
+_c = ctypes
+_SIGS = {
+    "bfa_compile": (_c.c_int, [_c.c_char_p, _c.POINTER(_c.c_void_p)]),
+    "bfa_free": (None, [_c.c_void_p]),
+    "bfa_info_get": (_c.c_int, [_c.c_void_p, _c.c_void_p]),
+    "bfa_set_option": (_c.c_int, [_c.c_void_p, _c.c_char_p, _c.c_int64]),
+    "bfa_count": (_c.c_uint64, [_c.c_void_p, _c.c_int]),
+    "bfa_eval": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p]),
+    "bfa_count_range": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_void_p]),
+    "bfa_eval_range": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_void_p,
+                                  _c.c_void_p]),
+    "bfa_fill_generators": (_c.c_int, [_c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
+    "bfa_eval_materialised": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p]),
+    "bfa_popcount": (_c.c_int, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_void_p]),
+    "bfa_peak_lop3": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
+    "bfa_last_launch_json": (_c.c_int, [_c.c_char_p, _c.c_size_t]),
+    "bfa_dump": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t]),
+    "bfa_jit_cubin": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_size_t]),
+    "bfa_last_error": (_c.c_char_p, []),
+    "bfa_version": (_c.c_char_p, []),
+}
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("max_var_id", ctypes.c_int32), ("const_value", ctypes.c_int32),
+                ("tree_nodes", ctypes.c_uint64), ("gates", ctypes.c_uint32), ("luts", ctypes.c_uint32),
+                ("support", ctypes.c_uint32), ("lets", ctypes.c_uint32)]
+
+
+class BfaError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"bfa error {code}: {msg}")
+        self.code = code
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} is not built: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                              "(libbfa has no CPU fallback)")
+        lib = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(rc: int):
+    if rc < 0:
+        raise BfaError(rc, _load().bfa_last_error().decode(errors="replace"))
+    return rc
+
+
+def version() -> str:
+    return _load().bfa_version().decode()
+
+
+def words_for(n: int) -> int:
+    """u64 words of a full DNF vector of n variables (include/bfa.h)."""
+    return max(1, 1 << max(n - 6, 0))
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _u64_out(out, numel):
+    import torch
+    if out is None:
+        return torch.empty(numel, dtype=torch.int64, device="cuda")
+    if out.dtype not in (torch.int64, torch.uint64) or not out.is_cuda or out.numel() < numel or not out.is_contiguous():
+        raise BfaError(BFA_E_ARG, f"output must be a contiguous CUDA int64 tensor of >= {numel} elements")
+    return out
+
+
+def last_launch() -> dict:
+    buf = ctypes.create_string_buffer(1 << 16)
+    _check(_load().bfa_last_launch_json(buf, len(buf)))
+    return json.loads(buf.value.decode())
+
+
+class Program:
+    """A compiled Boolean program (bfa_compile).  Grammar: include/bfa.h."""
+
+    def __init__(self, text: str):
+        lib = _load()
+        h = ctypes.c_void_p()
+        _check(lib.bfa_compile(text.encode(), ctypes.byref(h)))
+        self._h = h
+        self.text = text
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.bfa_free(self._h)
+            self._h = None
+
+    @property
+    def info(self) -> dict:
+        i = _Info()
+        _check(_load().bfa_info_get(self._h, ctypes.byref(i)))
+        return {f: getattr(i, f) for f, _ in _Info._fields_}
+
+    def set_option(self, key: str, value: int) -> "Program":
+        _check(_load().bfa_set_option(self._h, key.encode(), int(value)))
+        return self
+
+    # ---- register-synthesised mode
+    def count(self, n: int) -> int:
+        """bfa_count: number of models over all 2^n valuations (synchronous)."""
+        c = _load().bfa_count(self._h, n)
+        if c == UINT64_MAX:
+            raise BfaError(_err_code(), _load().bfa_last_error().decode(errors="replace"))
+        return int(c)
+
+    def count_range(self, n: int, lo: int, hi: int, out=None, stream=None):
+        """bfa_count_range: models in [lo, hi) into a 1-element device tensor (async)."""
+        out = _u64_out(out, 1)
+        _check(_load().bfa_count_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+        return out
+
+    def eval(self, n: int, out=None):
+        """bfa_eval: the full-DNF vector as words_for(n) device int64 words (synchronous)."""
+        out = _u64_out(out, words_for(n))
+        _check(_load().bfa_eval(self._h, n, ctypes.c_void_p(out.data_ptr())))
+        return out
+
+    def eval_range(self, n: int, lo: int, hi: int, out=None, count_out=None, stream=None):
+        """bfa_eval_range: slice [lo, hi) of the vector (async); optional fused count."""
+        out = _u64_out(out, max(1, (hi - lo + 63) // 64))
+        cp = ctypes.c_void_p(count_out.data_ptr()) if count_out is not None else None
+        _check(_load().bfa_eval_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), cp, _stream(stream)))
+        return out
+
+    # ---- materialised mode
+    def eval_materialised(self, n: int, variant: int = 0, out=None, count_out=None, stream=None):
+        out = _u64_out(out, words_for(n))
+        cp = ctypes.c_void_p(count_out.data_ptr()) if count_out is not None else None
+        _check(_load().bfa_eval_materialised(self._h, n, variant, ctypes.c_void_p(out.data_ptr()), cp,
+                                             _stream(stream)))
+        return out
+
+    # ---- introspection (no GPU needed)
+    def dump(self, what: int = 0, n: int = 0) -> str:
+        lib = _load()
+        size = _check(lib.bfa_dump(self._h, what, n, None, 0))
+        buf = ctypes.create_string_buffer(size + 1)
+        _check(lib.bfa_dump(self._h, what, n, buf, size + 1))
+        return buf.value.decode()
+
+    def jit_cubin(self, what: int = 1, n: int = 0) -> bytes:
+        lib = _load()
+        size = _check(lib.bfa_jit_cubin(self._h, what, n, None, 0))
+        buf = ctypes.create_string_buffer(size)
+        _check(lib.bfa_jit_cubin(self._h, what, n, buf, size))
+        return buf.raw
+
+
+def _err_code() -> int:
+    msg = _load().bfa_last_error().decode()
+    for code, key in ((BFA_E_RANGE, "outside"), (BFA_E_RANGE, "needs n"), (BFA_E_CUDA, "CUDA"),
+                      (BFA_E_CUDA, "device"), (BFA_E_JIT, "NVRTC"), (BFA_E_JIT, "cuModule")):
+        if key in msg:
+            return code
+    return BFA_E_ARG
+
+
+def fill_generators(n: int, rows: int | None = None, out=None, stream=None):
+    """bfa_fill_generators: the table S of free generators (rows x words_for(n))."""
+    rows = n if rows is None else rows
+    out = _u64_out(out, rows * words_for(n))
+    _check(_load().bfa_fill_generators(n, rows, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
+def popcount(vec, count_out=None, stream=None):
+    count_out = _u64_out(count_out, 1)
+    _check(_load().bfa_popcount(ctypes.c_void_p(vec.data_ptr()), vec.numel(),
+                                ctypes.c_void_p(count_out.data_ptr()), _stream(stream)))
+    return count_out
+
+
+def peak_lop3(blocks: int, threads: int, iters: int, sink, stream=None):
+    _check(_load().bfa_peak_lop3(blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream(stream)))

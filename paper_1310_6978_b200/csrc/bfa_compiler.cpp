@@ -1,0 +1,759 @@
+// bfa_compiler.cpp -- parser, gate DAG with Reduction, LUT3 mapping and CUDA
+// code generation for libbfa.  See bfa_compiler.hpp for the pipeline.
+#include "bfa_compiler.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <sstream>
+
+namespace bfa {
+
+// ============================================================== Dag
+Dag::Dag() {
+  nodes.push_back(Node{NK_CONST, 0, 0, 0, 0u});  // node 0: the word 0 (literal 1 = all ones)
+  word_table_[0u] = 0;
+}
+
+Lit Dag::word(uint32_t w) {
+  bool neg = (w & 1u) != 0;           // normalise: stored word has bit 0 clear
+  uint32_t key = neg ? ~w : w;
+  auto it = word_table_.find(key);
+  if (it != word_table_.end()) return mk_lit(it->second, neg);
+  uint32_t id = (uint32_t)nodes.size();
+  nodes.push_back(Node{NK_CONST, 0, 0, 0, key});
+  word_table_[key] = id;
+  return mk_lit(id, neg);
+}
+
+Lit Dag::var(uint32_t id) {
+  auto it = var_table_.find(id);
+  if (it != var_table_.end()) return mk_lit(it->second, false);
+  uint32_t n = (uint32_t)nodes.size();
+  nodes.push_back(Node{NK_VAR, 0, 0, 0, id});
+  var_table_[id] = n;
+  return mk_lit(n, false);
+}
+
+// Bitwise application of a 2-input truth table (bit a+2b) to two words.
+static inline uint32_t apply2(uint8_t tt, uint32_t A, uint32_t B) {
+  uint32_t r = 0;
+  if (tt & 1) r |= ~A & ~B;
+  if (tt & 2) r |= A & ~B;
+  if (tt & 4) r |= ~A & B;
+  if (tt & 8) r |= A & B;
+  return r;
+}
+
+// Negate input a / input b of a 2-input truth table.
+static inline uint8_t tt_neg_a(uint8_t tt) { return (uint8_t)(((tt & 0x5) << 1) | ((tt & 0xA) >> 1)); }
+static inline uint8_t tt_neg_b(uint8_t tt) { return (uint8_t)(((tt & 0x3) << 2) | ((tt & 0xC) >> 2)); }
+static inline uint8_t tt_swap(uint8_t tt) { return (uint8_t)((tt & 0x9) | ((tt & 0x2) << 1) | ((tt & 0x4) >> 1)); }
+
+// The constructor is the Reduction step: constants are
+// propagated, x op x and x op ~x are folded, NOTs are absorbed into the
+// consumer's truth table, and structurally equal gates are shared.
+Lit Dag::gate(uint8_t tt, Lit la, Lit lb) {
+  tt &= 0xF;
+  if (lit_neg(la)) tt = tt_neg_a(tt);
+  if (lit_neg(lb)) tt = tt_neg_b(tt);
+  uint32_t a = lit_node(la), b = lit_node(lb);
+  const Node& na = nodes[a];
+  const Node& nb = nodes[b];
+  if (na.kind == NK_CONST && nb.kind == NK_CONST) return word(apply2(tt, na.val, nb.val));
+  // a is the Boolean constant 0: f(0, b) = b ? tt[2] : tt[0]
+  auto unary = [&](int f0, int f1, Lit x) -> Lit {
+    if (f0 == f1) return f0 ? const1() : const0();
+    return f1 ? x : (x ^ 1u);
+  };
+  if (na.kind == NK_CONST && na.val == 0 && a == 0) return unary(tt & 1, (tt >> 2) & 1, mk_lit(b, false));
+  if (nb.kind == NK_CONST && nb.val == 0 && b == 0) return unary(tt & 1, (tt >> 1) & 1, mk_lit(a, false));
+  if (a == b) return unary(tt & 1, (tt >> 3) & 1, mk_lit(a, false));
+  // truth tables that ignore an input
+  if ((tt & 0x3) == ((tt >> 2) & 0x3)) return unary(tt & 1, (tt >> 1) & 1, mk_lit(a, false));
+  if ((tt & 0x5) == ((tt >> 1) & 0x5)) return unary(tt & 1, (tt >> 2) & 1, mk_lit(b, false));
+  if (a > b) { std::swap(a, b); tt = tt_swap(tt); }
+  bool neg = false;
+  if (tt & 1) { tt = (uint8_t)(~tt & 0xF); neg = true; }  // normalise f(0,0) = 0
+  uint64_t key = ((uint64_t)tt << 58) ^ ((uint64_t)a << 29) ^ (uint64_t)b;
+  auto it = gate_table_.find(key);
+  if (it != gate_table_.end()) return mk_lit(it->second, neg);
+  uint32_t id = (uint32_t)nodes.size();
+  nodes.push_back(Node{NK_GATE, tt, a, b, 0});
+  gate_table_[key] = id;
+  return mk_lit(id, neg);
+}
+
+size_t Dag::gate_count() const {
+  size_t g = 0;
+  for (const Node& n : nodes) g += n.kind == NK_GATE;
+  return g;
+}
+
+// ============================================================== parser
+// An independent recursive-descent parser for the grammar of include/bfa.h.
+namespace {
+
+enum Tok { EOF_, SEP, NOT_, AND_, XOR_, OR_, IMP_, IFF_, LP, RP, EQ, VAR, NAME, ZERO, ONE, LET };
+
+struct Lexer {
+  const std::string& s;
+  size_t i = 0;
+  int line = 1, col = 1, depth = 0;
+  Tok tok = EOF_;
+  std::string text;
+  long long ival = 0;
+  int tline = 1, tcol = 1;
+  std::string err;
+
+  explicit Lexer(const std::string& src) : s(src) {}
+
+  bool fail(const std::string& msg) {
+    if (err.empty()) err = std::to_string(tline) + ":" + std::to_string(tcol) + ": " + msg;
+    tok = EOF_;
+    return false;
+  }
+  char at(size_t k) const { return k < s.size() ? s[k] : '\0'; }
+  void adv(size_t k) { i += k; col += (int)k; }
+
+  bool next() {
+    for (;;) {
+      char c = at(i);
+      if (c == '#') { while (at(i) && at(i) != '\n') adv(1); continue; }
+      if (c == ' ' || c == '\t' || c == '\r') { adv(1); continue; }
+      if (c == '\n' && depth > 0) { i++; line++; col = 1; continue; }
+      break;
+    }
+    tline = line; tcol = col;
+    char c = at(i);
+    switch (c) {
+      case '\0': tok = EOF_; return true;
+      case '\n': i++; line++; col = 1; tok = SEP; return true;
+      case ';': adv(1); tok = SEP; return true;
+      case '~': adv(1); tok = NOT_; return true;
+      case '&': adv(1); tok = AND_; return true;
+      case '^': adv(1); tok = XOR_; return true;
+      case '|': adv(1); tok = OR_; return true;
+      case '(': adv(1); depth++; tok = LP; return true;
+      case ')': adv(1); if (depth) depth--; tok = RP; return true;
+      case '=': adv(1); tok = EQ; return true;
+      default: break;
+    }
+    if (c == '-' && at(i + 1) == '>') { adv(2); tok = IMP_; return true; }
+    if (c == '<' && at(i + 1) == '-' && at(i + 2) == '>') { adv(3); tok = IFF_; return true; }
+    if (std::isdigit((unsigned char)c)) {
+      size_t k = i;
+      while (std::isdigit((unsigned char)at(k))) k++;
+      std::string num = s.substr(i, k - i);
+      if (num == "0") tok = ZERO;
+      else if (num == "1") tok = ONE;
+      else return fail("only the constants 0 and 1 are allowed");
+      adv(k - i);
+      return true;
+    }
+    if (std::isalpha((unsigned char)c) || c == '_') {
+      size_t k = i;
+      while (std::isalnum((unsigned char)at(k)) || at(k) == '_') k++;
+      text = s.substr(i, k - i);
+      adv(k - i);
+      bool is_var = text.size() >= 2 && text[0] == 'x' &&
+                    std::all_of(text.begin() + 1, text.end(), [](char ch) { return std::isdigit((unsigned char)ch); });
+      if (is_var) {
+        ival = 0;
+        for (size_t q = 1; q < text.size() && ival <= 1000000; q++) ival = ival * 10 + (text[q] - '0');
+        tok = VAR;
+      } else {
+        tok = text == "let" ? LET : NAME;
+      }
+      return true;
+    }
+    return fail(std::string("unexpected character '") + c + "'");
+  }
+};
+
+struct Parser {
+  Lexer lx;
+  Parsed* P;
+  std::unordered_map<std::string, Lit> names;
+
+  Parser(const std::string& src, Parsed* out) : lx(src), P(out) {}
+  bool ok() const { return lx.err.empty(); }
+
+  // Balanced reduction of an operand list (n-ary & / | and the constraint conjunction).
+  Lit reduce_balanced(std::vector<Lit>& v, bool is_and) {
+    while (v.size() > 1) {
+      std::vector<Lit> nxt;
+      for (size_t k = 0; k + 1 < v.size(); k += 2)
+        nxt.push_back(is_and ? P->dag.AND(v[k], v[k + 1]) : P->dag.OR(v[k], v[k + 1]));
+      if (v.size() & 1) nxt.push_back(v.back());
+      v.swap(nxt);
+    }
+    return v[0];
+  }
+
+  Lit atom() {
+    Dag& d = P->dag;
+    switch (lx.tok) {
+      case VAR: {
+        if (lx.ival > 62) { lx.fail("variable id " + std::to_string(lx.ival) + " > 62"); return 0; }
+        int id = (int)lx.ival;
+        P->max_var = std::max(P->max_var, id);
+        P->support_mask |= 1ull << id;
+        P->tree_nodes++;
+        lx.next();
+        return d.var((uint32_t)id);
+      }
+      case ZERO: P->tree_nodes++; lx.next(); return d.const0();
+      case ONE: P->tree_nodes++; lx.next(); return d.const1();
+      case NAME: {
+        auto it = names.find(lx.text);
+        if (it == names.end()) { lx.fail("name '" + lx.text + "' used before definition"); return 0; }
+        P->tree_nodes++;
+        lx.next();
+        return it->second;
+      }
+      case LP: {
+        lx.next();
+        Lit e = expr();
+        if (!ok()) return 0;
+        if (lx.tok != RP) { lx.fail("expected ')'"); return 0; }
+        lx.next();
+        return e;
+      }
+      default: lx.fail("expected an operand"); return 0;
+    }
+  }
+  Lit unary() {
+    if (lx.tok == NOT_) {
+      lx.next();
+      Lit a = unary();
+      P->tree_nodes++;
+      return a ^ 1u;
+    }
+    return atom();
+  }
+  Lit chain(Tok op, bool is_and, Lit (Parser::*sub)()) {
+    Lit first = (this->*sub)();
+    if (!ok() || lx.tok != op) return first;
+    std::vector<Lit> ops{first};
+    while (ok() && lx.tok == op) {
+      lx.next();
+      ops.push_back((this->*sub)());
+      P->tree_nodes++;
+    }
+    if (!ok()) return 0;
+    return reduce_balanced(ops, is_and);
+  }
+  Lit and_() { return chain(AND_, true, &Parser::unary); }
+  Lit xor_() {
+    Lit a = and_();
+    while (ok() && lx.tok == XOR_) { lx.next(); Lit b = and_(); P->tree_nodes++; a = P->dag.XOR(a, b); }
+    return a;
+  }
+  Lit or_() { return chain(OR_, false, &Parser::xor_); }
+  Lit imp() {
+    Lit a = or_();
+    if (!ok() || lx.tok != IMP_) return a;
+    lx.next();
+    Lit b = imp();
+    P->tree_nodes++;
+    return P->dag.IMP(a, b);
+  }
+  Lit expr() {
+    Lit a = imp();
+    while (ok() && lx.tok == IFF_) { lx.next(); Lit b = imp(); P->tree_nodes++; a = P->dag.IFF(a, b); }
+    return a;
+  }
+
+  bool bind(const std::string& name, Lit v) {
+    if (names.count(name)) return lx.fail("name '" + name + "' redefined");
+    names[name] = v;
+    P->lets++;
+    return true;
+  }
+
+  bool program() {
+    std::vector<Lit> constraints;
+    lx.next();
+    while (ok() && lx.tok != EOF_) {
+      if (lx.tok == SEP) { lx.next(); continue; }
+      if (lx.tok == LET) {
+        lx.next();
+        if (lx.tok != NAME) return lx.fail("expected a name after 'let'");
+        std::string name = lx.text;
+        lx.next();
+        if (lx.tok != EQ) return lx.fail("expected '='");
+        lx.next();
+        Lit v = expr();
+        if (!ok()) return false;
+        if (!bind(name, v)) return false;
+      } else if (lx.tok == NAME) {
+        // one-token lookahead for NAME '=' : snapshot the lexer
+        Lexer save = lx;
+        std::string name = lx.text;
+        lx.next();
+        if (ok() && lx.tok == EQ) {
+          lx.next();
+          Lit v = expr();
+          if (!ok()) return false;
+          if (!bind(name, v)) return false;
+          constraints.push_back(v);
+        } else {
+          if (!ok()) return false;
+          lx.i = save.i; lx.line = save.line; lx.col = save.col; lx.depth = save.depth;
+          lx.tok = save.tok; lx.text = save.text; lx.tline = save.tline; lx.tcol = save.tcol;
+          Lit v = expr();
+          if (!ok()) return false;
+          constraints.push_back(v);
+        }
+      } else {
+        Lit v = expr();
+        if (!ok()) return false;
+        constraints.push_back(v);
+      }
+      if (!ok()) return false;
+      if (lx.tok != SEP && lx.tok != EOF_) return lx.fail("expected ';' or end of line");
+    }
+    if (!ok()) return false;
+    if (constraints.empty()) {
+      P->root = P->dag.const1();
+    } else {
+      P->tree_nodes += constraints.size() - 1;
+      P->root = reduce_balanced(constraints, true);
+    }
+    return true;
+  }
+};
+
+}  // namespace
+
+int parse_program(const std::string& text, Parsed* out, std::string* err) {
+  *out = Parsed();
+  Parser ps(text, out);
+  if (!ps.program()) {
+    if (err) *err = ps.lx.err.empty() ? "parse error" : ps.lx.err;
+    return -1;
+  }
+  return 0;
+}
+
+// ============================================================== rebuild (specialise)
+// Rebuild the cone of `root` from `src` into `dst`, substituting every
+// variable by subst[id] (a literal of dst).  dst.gate() re-runs the Reduction
+// so substituted constants propagate (cofactoring).
+static Lit rebuild(const Dag& src, Lit root, const std::vector<Lit>& subst, Dag& dst,
+                   std::vector<Lit>& memo, std::vector<uint8_t>& done) {
+  std::vector<uint32_t> stack{lit_node(root)};
+  while (!stack.empty()) {
+    uint32_t n = stack.back();
+    if (done[n]) { stack.pop_back(); continue; }
+    const Node& nd = src.nodes[n];
+    if (nd.kind == NK_CONST) {
+      memo[n] = n == 0 ? dst.const0() : dst.word(nd.val);
+      done[n] = 1; stack.pop_back(); continue;
+    }
+    if (nd.kind == NK_VAR) {
+      memo[n] = subst[nd.val];
+      done[n] = 1; stack.pop_back(); continue;
+    }
+    if (!done[nd.a]) { stack.push_back(nd.a); continue; }
+    if (!done[nd.b]) { stack.push_back(nd.b); continue; }
+    memo[n] = dst.gate(nd.tt, memo[nd.a], memo[nd.b]);
+    done[n] = 1;
+    stack.pop_back();
+  }
+  return memo[lit_node(root)] ^ (root & 1u);
+}
+
+// ============================================================== LUT3 mapping
+namespace {
+
+struct Cut {
+  uint32_t leaf[3];
+  uint8_t n;
+  uint8_t tt;   // over slots (0xF0, 0xCC, 0xAA)
+  float cost;
+};
+
+constexpr uint8_t kPat[3] = {0xF0, 0xCC, 0xAA};
+
+inline uint8_t apply3(uint8_t tt, uint8_t x, uint8_t y, uint8_t z) {
+  uint8_t r = 0;
+  for (int k = 0; k < 8; k++) {
+    if (!((tt >> k) & 1)) continue;
+    uint8_t m = (uint8_t)(((k & 4) ? x : ~x) & ((k & 2) ? y : ~y) & ((k & 1) ? z : ~z));
+    r |= m;
+  }
+  return r;
+}
+
+// expand cut c to the slot patterns of the merged leaf list L
+inline uint8_t expand(const Cut& c, const uint32_t* L, int nl) {
+  uint8_t X[3] = {0, 0, 0};
+  for (int j = 0; j < c.n; j++)
+    for (int q = 0; q < nl; q++)
+      if (L[q] == c.leaf[j]) X[j] = kPat[q];
+  return apply3(c.tt, X[0], X[1], X[2]);
+}
+
+}  // namespace
+
+MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
+                   const std::vector<uint8_t>& var_level, const double weights[4]) {
+  const size_t N = dag.nodes.size();
+  MapResult res;
+  res.node_level.assign(N, 0);
+  std::vector<uint8_t> in_cone(N, 0);
+  std::vector<uint32_t> fanout(N, 0);
+  {
+    std::vector<uint32_t> st;
+    for (Lit o : outputs) { st.push_back(lit_node(o)); fanout[lit_node(o)]++; }
+    while (!st.empty()) {
+      uint32_t n = st.back(); st.pop_back();
+      if (in_cone[n]) continue;
+      in_cone[n] = 1;
+      const Node& nd = dag.nodes[n];
+      if (nd.kind == NK_GATE) {
+        fanout[nd.a]++; fanout[nd.b]++;
+        st.push_back(nd.a); st.push_back(nd.b);
+      }
+    }
+  }
+  for (size_t n = 0; n < N; n++) {
+    const Node& nd = dag.nodes[n];
+    if (nd.kind == NK_VAR) res.node_level[n] = var_level[nd.val];
+    else if (nd.kind == NK_GATE) res.node_level[n] = std::max(res.node_level[nd.a], res.node_level[nd.b]);
+  }
+  const int kMaxCuts = 8;
+  std::vector<std::vector<Cut>> cuts(N);
+  std::vector<float> af(N, 0.f);
+  auto leaf_share = [&](uint32_t l) -> float {
+    return dag.nodes[l].kind == NK_GATE ? af[l] / (float)std::max<uint32_t>(1, fanout[l]) : 0.f;
+  };
+  for (size_t n = 0; n < N; n++) {
+    if (!in_cone[n]) continue;
+    const Node& nd = dag.nodes[n];
+    Cut triv{{(uint32_t)n, 0, 0}, 1, 0xF0, 0.f};
+    if (nd.kind != NK_GATE) { cuts[n].push_back(triv); continue; }
+    std::vector<Cut> cand;
+    for (const Cut& ca : cuts[nd.a]) {
+      for (const Cut& cb : cuts[nd.b]) {
+        uint32_t L[6]; int nl = 0;
+        for (int j = 0; j < ca.n; j++) L[nl++] = ca.leaf[j];
+        for (int j = 0; j < cb.n; j++) {
+          bool dup = false;
+          for (int q = 0; q < nl; q++) dup |= L[q] == cb.leaf[j];
+          if (!dup) L[nl++] = cb.leaf[j];
+        }
+        if (nl > 3) continue;
+        std::sort(L, L + nl);
+        Cut c{{0, 0, 0}, (uint8_t)nl, 0, 0.f};
+        for (int q = 0; q < nl; q++) c.leaf[q] = L[q];
+        uint8_t A = expand(ca, L, nl), B = expand(cb, L, nl);
+        uint8_t r = 0;
+        if (nd.tt & 1) r |= (uint8_t)(~A & ~B);
+        if (nd.tt & 2) r |= (uint8_t)(A & ~B);
+        if (nd.tt & 4) r |= (uint8_t)(~A & B);
+        if (nd.tt & 8) r |= (uint8_t)(A & B);
+        c.tt = r;
+        float cost = (float)weights[res.node_level[n]];
+        for (int q = 0; q < nl; q++) cost += leaf_share(L[q]);
+        c.cost = cost;
+        bool dup = false;
+        for (const Cut& e : cand)
+          if (e.n == c.n && std::equal(e.leaf, e.leaf + e.n, c.leaf)) { dup = true; break; }
+        if (!dup) cand.push_back(c);
+      }
+    }
+    std::stable_sort(cand.begin(), cand.end(), [](const Cut& x, const Cut& y) {
+      if (x.cost != y.cost) return x.cost < y.cost;
+      return x.n < y.n;
+    });
+    if ((int)cand.size() > kMaxCuts) cand.resize(kMaxCuts);
+    af[n] = cand.empty() ? (float)weights[res.node_level[n]] : cand[0].cost;
+    cuts[n] = cand;
+    cuts[n].push_back(triv);
+  }
+  // cover extraction from the outputs (reverse topological order)
+  std::vector<uint8_t> req(N, 0);
+  for (Lit o : outputs) req[lit_node(o)] = 1;
+  for (size_t k = N; k-- > 0;) {
+    if (!req[k] || dag.nodes[k].kind != NK_GATE) continue;
+    const Cut& c = cuts[k][0];
+    Lut lut{};
+    lut.root = (uint32_t)k;
+    lut.nin = c.n;
+    for (int q = 0; q < 3; q++) lut.in[q] = q < c.n ? c.leaf[q] : c.leaf[0];
+    lut.imm = c.tt;
+    lut.level = res.node_level[k];
+    res.luts.push_back(lut);
+    for (int q = 0; q < c.n; q++) req[c.leaf[q]] = 1;
+  }
+  std::reverse(res.luts.begin(), res.luts.end());
+  return res;
+}
+
+// ============================================================== codegen
+namespace {
+
+constexpr uint32_t kLane[5] = {0xAAAAAAAAu, 0xCCCCCCCCu, 0xF0F0F0F0u, 0xFF00FF00u, 0xFFFF0000u};
+
+std::string hex32(uint32_t w) {
+  char b[16];
+  snprintf(b, sizeof b, "0x%08xu", w);
+  return b;
+}
+
+struct Emitter {
+  const Dag& d;
+  std::ostringstream& os;
+  Emitter(const Dag& dag, std::ostringstream& o) : d(dag), os(o) {}
+
+  std::string name(uint32_t n) const {
+    const Node& nd = d.nodes[n];
+    if (nd.kind == NK_CONST) return hex32(nd.val);
+    if (nd.kind == NK_VAR) return "v" + std::to_string(nd.val);
+    return "n" + std::to_string(n);
+  }
+  std::string operand(uint32_t n) const {
+    const Node& nd = d.nodes[n];
+    return (nd.kind == NK_CONST ? "\"n\"(" : "\"r\"(") + name(n) + ")";
+  }
+  std::string value(Lit l) const {
+    const Node& nd = d.nodes[lit_node(l)];
+    if (nd.kind == NK_CONST) return hex32(lit_neg(l) ? ~nd.val : nd.val);
+    return lit_neg(l) ? "(~" + name(lit_node(l)) + ")" : name(lit_node(l));
+  }
+  void lut(const Lut& L, const char* indent) {
+    char imm[8];
+    snprintf(imm, sizeof imm, "0x%02x", L.imm);
+    os << indent << "u32 " << name(L.root) << "; asm(\"lop3.b32 %0, %1, %2, %3, " << imm
+       << ";\" : \"=r\"(" << name(L.root) << ") : " << operand(L.in[0]) << ", " << operand(L.in[1])
+       << ", " << operand(L.in[2]) << ");\n";
+  }
+};
+
+const char* kPrelude =
+    "typedef unsigned int u32;\n"
+    "typedef unsigned long long u64;\n"
+    "struct __align__(16) u32x4 { u32 x, y, z, w; };\n"
+    "struct __align__(8) u32x2 { u32 x, y; };\n"
+    "__device__ __forceinline__ void bfa_block_sum(u64 acc, u64* count) {\n"
+    "  #pragma unroll\n"
+    "  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
+    "  __shared__ u64 red[32];\n"
+    "  const u32 tid = threadIdx.x;\n"
+    "  if ((tid & 31u) == 0) red[tid >> 5] = acc;\n"
+    "  __syncthreads();\n"
+    "  if (tid < 32u) {\n"
+    "    u64 v = tid < (blockDim.x >> 5) ? red[tid] : 0ull;\n"
+    "    #pragma unroll\n"
+    "    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);\n"
+    "    if (tid == 0 && v) atomicAdd(count, v);\n"
+    "  }\n"
+    "}\n";
+
+}  // namespace
+
+std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats) {
+  KernelStats st;
+  std::ostringstream os;
+  os << "// generated by libbfa: " << (spec.mode == KM_COUNT ? "count" : "eval")
+     << (spec.generic ? " generic" : " specialised") << " s=" << spec.slot_bits << " t=" << spec.thread_bits
+     << " m=" << spec.inner_bits << "\n" << kPrelude;
+
+  const int S = spec.generic ? 1 : (1 << spec.slot_bits);
+  const int s = spec.generic ? 0 : spec.slot_bits;
+  const int t = spec.thread_bits, m = spec.inner_bits;
+  const bool want_count = spec.mode == KM_COUNT || spec.fuse_count;
+
+  // roles of word-index bit p = v - 5:
+  //   generic:     every v >= 5 is level 3, read from w
+  //   specialised: p < s slot (constant per slot), < s+t thread (1),
+  //                < s+t+m inner (3), else outer (2)
+  auto level_of = [&](int v) -> int {
+    if (spec.materialised) return 3;
+    if (v < 5) return 0;
+    int p = v - 5;
+    if (spec.generic) return 3;
+    if (p < s) return 0;
+    if (p < s + t) return 1;
+    if (p < s + t + m) return 3;
+    return 2;
+  };
+  Dag D;
+  std::vector<Lit> outs;
+  std::vector<uint8_t> done(prog.dag.nodes.size());
+  std::vector<Lit> memo(prog.dag.nodes.size());
+  for (int slot = 0; slot < S; slot++) {
+    std::vector<Lit> subst(64, 0);
+    for (int v = 0; v < 64; v++) {
+      if (v < 5 && !spec.materialised) subst[v] = D.word(kLane[v]);
+      else if (!spec.generic && v - 5 < s) subst[v] = ((slot >> (v - 5)) & 1) ? D.const1() : D.const0();
+      else subst[v] = D.var((uint32_t)v);
+    }
+    std::fill(done.begin(), done.end(), 0);
+    outs.push_back(rebuild(prog.dag, prog.root, subst, D, memo, done));
+  }
+  std::vector<uint8_t> var_level(64, 0);
+  for (int v = 0; v < 64; v++) var_level[v] = (uint8_t)level_of(v);
+  const double iters_inner = (double)(1u << m);
+  const double w[4] = {0.0, 1e-4, spec.generic ? 1.0 : 1.0 / iters_inner, 1.0};
+  MapResult mr = map_luts(D, outs, var_level, w);
+
+  // which variables are referenced (as LUT inputs or outputs)
+  std::vector<uint8_t> used(64, 0);
+  auto mark = [&](uint32_t n) { if (D.nodes[n].kind == NK_VAR) used[D.nodes[n].val] = 1; };
+  for (const Lut& L : mr.luts) for (int q = 0; q < 3; q++) mark(L.in[q]);
+  for (Lit o : outs) mark(lit_node(o));
+
+  Emitter E(D, os);
+  auto emit_level = [&](int lvl, const char* ind) {
+    uint32_t c = 0;
+    for (const Lut& L : mr.luts) if (L.level == lvl) { E.lut(L, ind); c++; }
+    return c;
+  };
+
+  if (spec.generic && spec.materialised) {
+    // the paper's table S in HBM: 128-bit loads of every
+    // generator row the program uses, the LOP3 body in registers, 128-bit store
+    os << "__device__ __forceinline__ u32 comp(const uint4& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }\n"
+       << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+       << "bfa_kernel(const u32* __restrict__ table, const u64 row_words, const u64 groups, u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "  u64 acc = 0;\n"
+       << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
+       << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < groups; k += stride) {\n";
+    for (int v = 0; v < 64; v++)
+      if (used[v])
+        os << "    const uint4 V" << v << " = __ldcs(reinterpret_cast<const uint4*>(table + " << v
+           << "ull * row_words) + k);\n";
+    os << "    u32 R[4];\n"
+       << "    #pragma unroll\n"
+       << "    for (int c = 0; c < 4; ++c) {\n";
+    for (int v = 0; v < 64; v++)
+      if (used[v]) os << "      const u32 v" << v << " = comp(V" << v << ", c);\n";
+    for (const Lut& L : mr.luts) E.lut(L, "      ");
+    st.luts_inner = (uint32_t)mr.luts.size();
+    os << "      R[c] = " << E.value(outs[0]) << ";\n"
+       << "    }\n";
+    if (spec.mode == KM_EVAL)
+      os << "    __stcs(reinterpret_cast<uint4*>(out) + k, make_uint4(R[0], R[1], R[2], R[3]));\n";
+    if (want_count) os << "    acc += __popc(R[0]) + __popc(R[1]) + __popc(R[2]) + __popc(R[3]);\n";
+    os << "  }\n";
+    if (want_count) os << "  bfa_block_sum(acc, count);\n";
+    os << "}\n";
+    st.words_per_iter = 4;
+    for (int v = 0; v < 64; v++) st.inner_vars += used[v];
+  } else if (spec.generic) {
+    os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+       << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "  u64 acc = 0;\n"
+       << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
+       << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += stride) {\n"
+       << "    const u64 w = w_begin + k;\n";
+    for (int v = 5; v < 64; v++)
+      if (used[v]) os << "    const u32 v" << v << " = 0u - (u32)((w >> " << (v - 5) << ") & 1ull);\n";
+    for (const Lut& L : mr.luts) E.lut(L, "    ");
+    st.luts_inner = (uint32_t)mr.luts.size();
+    os << "    const u32 r = (" << E.value(outs[0]) << ") & mask;\n";
+    if (spec.mode == KM_EVAL) os << "    out[k] = r;\n";
+    if (want_count) os << "    acc += __popc(r);\n";
+    os << "  }\n";
+    if (want_count) os << "  bfa_block_sum(acc, count);\n";
+    os << "}\n";
+    st.words_per_iter = 1;
+    for (int v = 5; v < 64; v++) st.inner_vars += used[v];
+  } else {
+    const int unit = s + t + m;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+       << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "  const u32 tid = threadIdx.x;\n"
+       << "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n"
+       << "  const u64 o_begin = b * q + (b < rr ? b : rr);\n"
+       << "  const u64 o_end = o_begin + q + (b < rr ? 1ull : 0ull);\n";
+    for (int v = 5; v < 64; v++)
+      if (used[v] && level_of(v) == 1) {
+        os << "  const u32 v" << v << " = 0u - ((tid >> " << (v - 5 - s) << ") & 1u);\n";
+        st.thread_vars++;
+      }
+    st.luts_thread = emit_level(1, "  ");
+    os << "  u64 acc = 0;\n"
+       << "  for (u64 o = o_begin; o < o_end; ++o) {\n"
+       << "    const u64 wo = A + (o << " << unit << ");\n";
+    for (int v = 5; v < 64; v++)
+      if (used[v] && level_of(v) == 2) {
+        os << "    const u32 v" << v << " = 0u - (u32)((wo >> " << (v - 5) << ") & 1ull);\n";
+        st.outer_vars++;
+      }
+    st.luts_outer = emit_level(2, "    ");
+    os << "    u32 acc32 = 0;\n"
+       << "    #pragma unroll 1\n"
+       << "    for (u32 i = 0; i < " << (1u << m) << "u; ++i) {\n";
+    for (int v = 5; v < 64; v++)
+      if (used[v] && level_of(v) == 3) {
+        int k = v - 5 - s - t;
+        os << "      const u32 v" << v << " = (u32)(((int)(i << " << (31 - k) << ")) >> 31);\n";
+        st.inner_vars++;
+      }
+    st.luts_inner = emit_level(3, "      ");
+    for (int sl = 0; sl < S; sl++) os << "      const u32 r" << sl << " = " << E.value(outs[sl]) << ";\n";
+    if (spec.mode == KM_EVAL) {
+      os << "      const u64 idx = (wo - out_base_w) + ((u64)i << " << (s + t) << ") + ((u64)tid << " << s << ");\n";
+      if (S == 1) os << "      out[idx] = r0;\n";
+      else if (S == 2) os << "      *reinterpret_cast<u32x2*>(out + idx) = u32x2{r0, r1};\n";
+      else
+        for (int g = 0; g < S; g += 4)
+          os << "      *reinterpret_cast<u32x4*>(out + idx + " << g << ") = u32x4{r" << g << ", r" << g + 1
+             << ", r" << g + 2 << ", r" << g + 3 << "};\n";
+    }
+    if (want_count) {
+      os << "      acc32 += ";
+      for (int sl = 0; sl < S; sl++) os << (sl ? " + " : "") << "__popc(r" << sl << ")";
+      os << ";\n";
+    }
+    os << "    }\n"
+       << "    acc += acc32;\n"
+       << "  }\n";
+    if (want_count) os << "  bfa_block_sum(acc, count);\n";
+    os << "}\n";
+    st.words_per_iter = (uint32_t)S;
+  }
+  if (stats) *stats = st;
+  return os.str();
+}
+
+std::string dump_ir(const Parsed& prog, uint32_t* n_luts) {
+  Dag D;
+  std::vector<Lit> subst(64);
+  for (int v = 0; v < 64; v++) subst[v] = D.var((uint32_t)v);
+  std::vector<uint8_t> done(prog.dag.nodes.size());
+  std::vector<Lit> memo(prog.dag.nodes.size());
+  Lit out = rebuild(prog.dag, prog.root, subst, D, memo, done);
+  std::vector<uint8_t> lv(64, 3);
+  const double w[4] = {0, 1, 1, 1};
+  MapResult mr = map_luts(D, {out}, lv, w);
+  std::unordered_map<uint32_t, int> idx;
+  std::ostringstream os;
+  auto opnd = [&](uint32_t n) -> std::string {
+    const Node& nd = D.nodes[n];
+    if (nd.kind == NK_CONST) { char b[16]; snprintf(b, sizeof b, "0x%08x", nd.val); return b; }
+    if (nd.kind == NK_VAR) return "x" + std::to_string(nd.val);
+    return "L" + std::to_string(idx.at(n));
+  };
+  int k = 0;
+  for (const Lut& L : mr.luts) {
+    idx[L.root] = k;
+    char imm[8];
+    snprintf(imm, sizeof imm, "0x%02x", L.imm);
+    os << "L" << k << " = lop3(" << opnd(L.in[0]) << ", " << opnd(L.in[1]) << ", " << opnd(L.in[2]) << ", "
+       << imm << ")\n";
+    k++;
+  }
+  os << "out = " << (lit_neg(out) ? "~" : "") << opnd(lit_node(out)) << "\n";
+  if (n_luts) *n_luts = (uint32_t)mr.luts.size();
+  return os.str();
+}
+
+}  // namespace bfa

@@ -1,0 +1,126 @@
+// bfa_compiler.hpp -- host-side compiler of libbfa.
+//
+// expression text --parse--> hash-consed gate DAG with constant propagation
+// (the paper's Translate + Reduction submodules)
+// --specialise--> per-slot cofactors with loop-level roles for the variables
+// --map--> 3-input LUT cover (one lop3.b32 per LUT, the "efficient computing
+// tree adapted to the actual parallel hardware")
+// --emit--> straight-line CUDA C++ for NVRTC (the paper's core is likewise
+// generated code compiled to binaries at run time).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace bfa {
+
+// A literal is (node << 1) | complement.
+using Lit = uint32_t;
+inline uint32_t lit_node(Lit l) { return l >> 1; }
+inline bool lit_neg(Lit l) { return l & 1u; }
+inline Lit mk_lit(uint32_t node, bool neg) { return (node << 1) | (neg ? 1u : 0u); }
+
+enum NodeKind : uint8_t { NK_CONST = 0, NK_VAR = 1, NK_GATE = 2 };
+
+// Gates are 2-input with a 4-bit truth table over POSITIVE node inputs:
+// bit (a + 2b) = f(a, b).  Complements live only on literals.  Constants are
+// 32-bit words (a word constant is a lane mask of the low variables); they are
+// normalised so that bit 0 of the stored word is 0.
+struct Node {
+  NodeKind kind;
+  uint8_t tt;       // GATE
+  uint32_t a, b;    // GATE inputs (node ids), a < b
+  uint32_t val;     // VAR: variable id (or role slot); CONST: word
+};
+
+class Dag {
+ public:
+  Dag();
+  std::vector<Node> nodes;
+
+  Lit const0() const { return mk_lit(0, false); }
+  Lit const1() const { return mk_lit(0, true); }
+  Lit word(uint32_t w);
+  Lit var(uint32_t id);
+  Lit gate(uint8_t tt, Lit a, Lit b);
+
+  Lit NOT(Lit a) { return a ^ 1u; }
+  Lit AND(Lit a, Lit b) { return gate(0x8, a, b); }
+  Lit OR(Lit a, Lit b) { return gate(0xE, a, b); }
+  Lit XOR(Lit a, Lit b) { return gate(0x6, a, b); }
+  Lit IMP(Lit a, Lit b) { return gate(0xD, a, b); }  // ~a | b : f(1,0) = 0 only
+  Lit IFF(Lit a, Lit b) { return gate(0x9, a, b); }
+
+  bool is_const(Lit l) const { return nodes[lit_node(l)].kind == NK_CONST; }
+  uint32_t const_word(Lit l) const {
+    uint32_t w = nodes[lit_node(l)].val;
+    return lit_neg(l) ? ~w : w;
+  }
+  size_t gate_count() const;
+
+ private:
+  std::unordered_map<uint64_t, uint32_t> gate_table_;
+  std::unordered_map<uint32_t, uint32_t> word_table_;
+  std::unordered_map<uint32_t, uint32_t> var_table_;
+};
+
+struct Parsed {
+  Dag dag;
+  Lit root = 0;
+  int max_var = -1;
+  uint64_t tree_nodes = 0;
+  uint32_t lets = 0;
+  uint64_t support_mask = 0;
+};
+
+// Parse `text` (grammar in include/bfa.h).  Returns 0 or -1 with "line:col: msg".
+int parse_program(const std::string& text, Parsed* out, std::string* err);
+
+// ---------------------------------------------------------------- mapping
+struct Lut {
+  uint32_t root;      // node id in the mapped DAG
+  uint8_t nin;        // leaves used (1..3)
+  uint32_t in[3];     // leaf node ids (VAR, CONST or GATE roots)
+  uint8_t imm;        // lop3 immLut over (in[0], in[1], in[2]) ~ (0xF0, 0xCC, 0xAA)
+  uint8_t level;      // loop level of the root
+};
+
+// Map the DAG (restricted to the cones of `outputs`) onto 3-input LUTs.
+// level_of_var(var id) gives each variable's loop level; constants are level
+// 0.  weights[level] is the relative execution frequency used by area flow.
+struct MapResult {
+  std::vector<Lut> luts;                 // topological order
+  std::vector<uint8_t> node_level;       // per node of the dag
+};
+MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
+                   const std::vector<uint8_t>& var_level, const double weights[4]);
+
+// ---------------------------------------------------------------- kernels
+enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1 };
+
+struct KernelSpec {
+  KernelMode mode = KM_COUNT;
+  bool generic = false;   // one word per thread-iteration, every variable from w
+  int slot_bits = 2;      // s
+  int thread_bits = 8;    // t
+  int inner_bits = 4;     // m
+  bool fuse_count = false;  // eval mode: also popcount
+  bool materialised = false;  // generic only: every generator word is LOADED from the
+                              // table S (128-bit loads, 4 words per thread-iteration)
+};
+
+struct KernelStats {
+  uint32_t luts_thread = 0, luts_outer = 0, luts_inner = 0;  // LUTs emitted per level
+  uint32_t inner_vars = 0, outer_vars = 0, thread_vars = 0;
+  uint32_t words_per_iter = 1;
+};
+
+// CUDA C++ source of one kernel variant (entry point "bfa_kernel").
+std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);
+
+// LUT cover IR text (bfa_dump what=0) and the plain cover size L.
+std::string dump_ir(const Parsed& prog, uint32_t* n_luts);
+
+}  // namespace bfa

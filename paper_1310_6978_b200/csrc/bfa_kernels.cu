@@ -1,0 +1,172 @@
+// bfa_kernels.cu -- ahead-of-time sm_100a kernels of libbfa:
+//   gen_fill   : materialise the generator table S (§4.1)
+//   vec_lut3   : one vector-algebra pass d = LOP3(a, b, c) over whole 2^n-bit
+//                vectors of Omega_n; the op is a kernel
+//                parameter, i.e. it lives in the constant bank
+//   popcount   : number of 1 bits of a materialised vector
+//   peak_lop3  : LOP3 issue-rate microbenchmark (the int-ALU denominator)
+// The register-mode kernels are generated per program and JIT-compiled
+// (bfa_compiler.cpp / bfa_runtime.cpp).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "bfa_kernels.hpp"
+
+namespace {
+
+typedef unsigned int u32;
+typedef unsigned long long u64;
+
+// lane masks of variables 0..4 inside a 32-bit word: bit j = (j >> v) & 1
+__device__ __forceinline__ u32 lane_mask(int v) {
+  return v == 0 ? 0xAAAAAAAAu : v == 1 ? 0xCCCCCCCCu : v == 2 ? 0xF0F0F0F0u : v == 3 ? 0xFF00FF00u : 0xFFFF0000u;
+}
+
+// S row v, 4 consecutive 32-bit words per thread (128-bit stores).
+// row_words = 32-bit words per row (multiple of 4).
+__global__ void __launch_bounds__(256) gen_fill_kernel(uint4* __restrict__ table, int n_rows, u64 row_words) {
+  const u64 groups = row_words >> 2;
+  const u64 total = groups * (u64)n_rows;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += stride) {
+    const int v = (int)(k / groups);
+    const u64 g = k - (u64)v * groups;
+    uint4 r;
+    if (v < 5) {
+      const u32 m = lane_mask(v);
+      r = make_uint4(m, m, m, m);
+    } else {
+      const u64 w = g << 2;  // word index of component 0
+      u32 c[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) c[j] = 0u - (u32)(((w + j) >> (v - 5)) & 1ull);
+      r = make_uint4(c[0], c[1], c[2], c[3]);
+    }
+    table[k] = r;
+  }
+}
+
+// f(a, b, c) with table bit (4a + 2b + c) = t[4a + 2b + c] (lop3 immLut order)
+__device__ __forceinline__ u32 mux3(u32 a, u32 b, u32 c, const u32* t) {
+  const u32 g00 = (c & t[1]) | (~c & t[0]), g01 = (c & t[3]) | (~c & t[2]);
+  const u32 g10 = (c & t[5]) | (~c & t[4]), g11 = (c & t[7]) | (~c & t[6]);
+  const u32 f0 = (b & g01) | (~b & g00), f1 = (b & g11) | (~b & g10);
+  return (a & f1) | (~a & f0);
+}
+
+__global__ void __launch_bounds__(256) vec_lut3_kernel(uint4* __restrict__ d, const uint4* __restrict__ a,
+                                                       const uint4* __restrict__ b, const uint4* __restrict__ c,
+                                                       u64 groups, u32 imm) {
+  u32 t[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) t[j] = 0u - ((imm >> j) & 1u);
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < groups; k += stride) {
+    const uint4 x = a[k], y = b[k], z = c[k];
+    // the 8-bit truth table is a runtime (warp-uniform) value: Shannon mux
+    // tree over (a, b, c) with the 8 table bits as 0/~0 masks -> 7 LOP3 per
+    // word, far below the HBM balance point of this pass.
+    uint4 r;
+    r.x = mux3(x.x, y.x, z.x, t);
+    r.y = mux3(x.y, y.y, z.y, t);
+    r.z = mux3(x.z, y.z, z.z, t);
+    r.w = mux3(x.w, y.w, z.w, t);
+    d[k] = r;
+  }
+}
+
+__device__ __forceinline__ void block_sum_add(u64 acc, u64* count) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+  __shared__ u64 red[32];
+  const u32 tid = threadIdx.x;
+  if ((tid & 31u) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid < 32u) {
+    u64 v = tid < (blockDim.x >> 5) ? red[tid] : 0ull;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (tid == 0 && v) atomicAdd(count, v);
+  }
+}
+
+// popcount over u64 words, 2 x u64 (128-bit) loads per thread-iteration
+__global__ void __launch_bounds__(256) popcount_kernel(const uint4* __restrict__ v, u64 pairs,
+                                                       const u64* __restrict__ tail, int has_tail, u64* count) {
+  u64 acc = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < pairs; k += stride) {
+    const uint4 x = v[k];
+    acc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+  }
+  if (has_tail && blockIdx.x == 0 && threadIdx.x == 0) acc += __popcll(*tail);
+  block_sum_add(acc, count);
+}
+
+// 8 independent lop3 chains, 32 ops each per unrolled step => 256 lop3 / iter
+__global__ void __launch_bounds__(256) peak_lop3_kernel(u32* sink, int iters, u32 seed) {
+  u32 x[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) x[j] = seed ^ (threadIdx.x * 0x9E3779B9u) ^ (j * 0x85EBCA6Bu);
+  const u32 y = seed * 3u + blockIdx.x, z = seed ^ 0x5bd1e995u;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+#pragma unroll
+      for (int j = 0; j < 8; j++)
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[j]) : "r"(y), "r"(z));
+    }
+  }
+  u32 acc = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) acc ^= x[j];
+  if (acc == 0x12345678u) sink[blockIdx.x] = acc;  // keep the chains alive
+}
+
+int grid_for(u64 items, int threads) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  u64 need = (items + threads - 1) / threads;
+  u64 cap = (u64)sms * 8;
+  if (need < 1) need = 1;
+  return (int)(need < cap ? need : cap);
+}
+
+}  // namespace
+
+namespace bfa_k {
+
+cudaError_t fill_generators(int n, int n_rows, uint64_t* table, cudaStream_t st) {
+  const u64 row_words32 = (n >= 7) ? (1ull << (n - 5)) : 4;  // padded to a 128-bit group
+  const u64 total = (row_words32 >> 2) * (u64)n_rows;
+  gen_fill_kernel<<<grid_for(total, 256), 256, 0, st>>>(reinterpret_cast<uint4*>(table), n_rows, row_words32);
+  return cudaGetLastError();
+}
+
+cudaError_t vec_lut3(uint64_t* d, const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t n_words64,
+                     uint32_t imm, cudaStream_t st) {
+  const u64 groups = n_words64 / 2;
+  vec_lut3_kernel<<<grid_for(groups, 256), 256, 0, st>>>(
+      reinterpret_cast<uint4*>(d), reinterpret_cast<const uint4*>(a), reinterpret_cast<const uint4*>(b),
+      reinterpret_cast<const uint4*>(c), groups, imm);
+  return cudaGetLastError();
+}
+
+cudaError_t popcount(const uint64_t* v, uint64_t n_words, uint64_t* count, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  const u64 pairs = n_words / 2;
+  const int has_tail = (int)(n_words & 1);
+  popcount_kernel<<<grid_for(pairs ? pairs : 1, 256), 256, 0, st>>>(
+      reinterpret_cast<const uint4*>(v), pairs, reinterpret_cast<const u64*>(v) + (n_words - 1), has_tail,
+      reinterpret_cast<u64*>(count));
+  return cudaGetLastError();
+}
+
+cudaError_t peak_lop3(int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st) {
+  peak_lop3_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
+  return cudaGetLastError();
+}
+
+}  // namespace bfa_k

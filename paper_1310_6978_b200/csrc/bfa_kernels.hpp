@@ -1,0 +1,15 @@
+// bfa_kernels.hpp -- host launchers of the ahead-of-time kernels (bfa_kernels.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace bfa_k {
+// table: n_rows rows of 2^(n-6) u64 words each (n >= 7)
+cudaError_t fill_generators(int n, int n_rows, uint64_t* table, cudaStream_t st);
+// d = LOP3(a, b, c; imm) over n_words64 u64 words (even)
+cudaError_t vec_lut3(uint64_t* d, const uint64_t* a, const uint64_t* b, const uint64_t* c, uint64_t n_words64,
+                     uint32_t imm, cudaStream_t st);
+// *count = popcount(v[0..n_words))
+cudaError_t popcount(const uint64_t* v, uint64_t n_words, uint64_t* count, cudaStream_t st);
+cudaError_t peak_lop3(int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st);
+}  // namespace bfa_k

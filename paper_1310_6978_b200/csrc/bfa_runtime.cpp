@@ -1,0 +1,698 @@
+// bfa_runtime.cpp -- the C ABI of libbfa (include/bfa.h): compile, JIT,
+// launch planning and the materialised mode.
+//
+// JIT: each (program, kernel variant) is emitted as CUDA C++ by the compiler,
+// compiled by NVRTC (statically linked) straight to an sm_100a cubin, and
+// loaded with the driver API into the current (primary) context; modules are
+// cached per device.  The paper's core is likewise generated code compiled to
+// binaries at run time.
+//
+// Launch planning: the 2^n valuations are 2^(n-5)
+// 32-bit words; a launch covers a word range [wlo, whi).  Its middle part,
+// aligned to units of 2^(s+t+m) words, runs on the specialised kernel (slots,
+// thread bits, inner-loop bits, outer-loop bits: see DESIGN.md); ragged heads
+// and tails and small problems run on the generic word-per-thread kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/bfa.h"
+#include "bfa_compiler.hpp"
+#include "bfa_kernels.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_last_launch = "{}";
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[2048];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+// ------------------------------------------------------------ driver API
+struct Driver {
+  CUresult (*ModuleLoadData)(CUmodule*, const void*) = nullptr;
+  CUresult (*ModuleGetFunction)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*LaunchKernel)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                           CUstream, void**, void**) = nullptr;
+  CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
+  CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
+  CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  bool ok = false;
+  std::string err;
+};
+
+Driver& drv() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto get = [](const char* sym, void** fp) -> bool {
+      cudaDriverEntryPointQueryResult q;
+      cudaError_t e = cudaGetDriverEntryPointByVersion(sym, fp, 12000, cudaEnableDefault, &q);
+      return e == cudaSuccess && q == cudaDriverEntryPointSuccess && *fp;
+    };
+    bool ok = get("cuModuleLoadData", (void**)&d.ModuleLoadData) &&
+              get("cuModuleGetFunction", (void**)&d.ModuleGetFunction) &&
+              get("cuLaunchKernel", (void**)&d.LaunchKernel) &&
+              get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.OccupancyMaxActiveBlocksPerMultiprocessor) &&
+              get("cuFuncGetAttribute", (void**)&d.FuncGetAttribute) &&
+              get("cuGetErrorString", (void**)&d.GetErrorString);
+    d.ok = ok;
+    if (!ok) d.err = "CUDA driver entry points unavailable (no driver / no device)";
+  });
+  return d;
+}
+
+std::string cu_str(CUresult r) {
+  const char* s = nullptr;
+  if (drv().GetErrorString) drv().GetErrorString(r, &s);
+  return s ? s : ("CUresult " + std::to_string((int)r));
+}
+
+// ------------------------------------------------------------ devices
+struct DevInfo {
+  int sms = 0;
+};
+
+int current_device(int* dev, DevInfo* info) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return set_err(BFA_E_CUDA, "no CUDA device available (%s); libbfa has no CPU fallback",
+                   e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  e = cudaGetDevice(dev);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  static std::mutex mu;
+  static std::map<int, DevInfo> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(*dev);
+  if (it == cache.end()) {
+    e = cudaFree(nullptr);  // make sure the primary context exists and is current
+    if (e != cudaSuccess) return set_err(BFA_E_CUDA, "context init: %s", cudaGetErrorString(e));
+    DevInfo di;
+    cudaDeviceGetAttribute(&di.sms, cudaDevAttrMultiProcessorCount, *dev);
+    it = cache.emplace(*dev, di).first;
+  }
+  if (info) *info = it->second;
+  if (!drv().ok) return set_err(BFA_E_CUDA, "%s", drv().err.c_str());
+  return BFA_OK;
+}
+
+// ------------------------------------------------------------ NVRTC
+int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "bfa_kernel.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return set_err(BFA_E_JIT, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17"};
+  r = nvrtcCompileProgram(prog, 3, opts);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    if (n) nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    if (log.size() > 1500) log = log.substr(0, 1500) + "...";
+    return set_err(BFA_E_JIT, "NVRTC: %s\n%s", nvrtcGetErrorString(r), log.c_str());
+  }
+  size_t sz = 0;
+  nvrtcGetCUBINSize(prog, &sz);
+  cubin->resize(sz);
+  nvrtcGetCUBIN(prog, cubin->data());
+  nvrtcDestroyProgram(&prog);
+  return BFA_OK;
+}
+
+// ------------------------------------------------------------ options
+struct Options {
+  int slot_bits = 2;
+  int thread_bits = 8;
+  int inner_bits = 4;
+  int blocks_per_sm = 0;
+  int force_generic = 0;
+  int engine = 0;
+};
+
+struct JitEntry {
+  std::string source;
+  std::vector<char> cubin;
+  bfa::KernelStats stats;
+  std::map<int, CUfunction> fn;   // per device
+  std::map<int, int> occupancy;   // blocks per SM per device
+  int regs = 0;
+};
+
+}  // namespace
+
+struct bfa_prog {
+  bfa::Parsed parsed;
+  bfa_info info{};
+  Options opt;
+  std::mutex mu;
+  std::map<std::string, std::unique_ptr<JitEntry>> jit;
+};
+
+namespace {
+
+std::string spec_key(const bfa::KernelSpec& s) {
+  std::ostringstream k;
+  k << s.mode << (s.generic ? 'g' : 's') << s.slot_bits << '.' << s.thread_bits << '.' << s.inner_bits
+    << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-');
+  return k.str();
+}
+
+// Compile (once) the variant `spec` of p; if dev >= 0 also load it on dev.
+int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntry** out, CUfunction* fn) {
+  bfa_prog* p = const_cast<bfa_prog*>(cp);
+  std::lock_guard<std::mutex> lk(p->mu);
+  std::string key = spec_key(spec);
+  auto it = p->jit.find(key);
+  if (it == p->jit.end()) {
+    auto e = std::make_unique<JitEntry>();
+    e->source = bfa::emit_kernel(p->parsed, spec, &e->stats);
+    int rc = nvrtc_compile(e->source, &e->cubin);
+    if (rc) return rc;
+    it = p->jit.emplace(key, std::move(e)).first;
+  }
+  JitEntry* e = it->second.get();
+  if (dev >= 0) {
+    auto f = e->fn.find(dev);
+    if (f == e->fn.end()) {
+      CUmodule mod;
+      CUresult r = drv().ModuleLoadData(&mod, e->cubin.data());
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleLoadData: %s", cu_str(r).c_str());
+      CUfunction k;
+      r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      int nb = 1;
+      drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 1 << spec.thread_bits, 0);
+      drv().FuncGetAttribute(&e->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
+      e->occupancy[dev] = std::max(1, nb);
+      f = e->fn.emplace(dev, k).first;
+    }
+    if (fn) *fn = f->second;
+  }
+  if (out) *out = e;
+  return BFA_OK;
+}
+
+int launch(CUfunction fn, unsigned grid, unsigned block, cudaStream_t st, void** args) {
+  CUresult r = drv().LaunchKernel(fn, grid, 1, 1, block, 1, 1, 0, (CUstream)st, args, nullptr);
+  if (r != CUDA_SUCCESS) return set_err(BFA_E_CUDA, "cuLaunchKernel: %s", cu_str(r).c_str());
+  return BFA_OK;
+}
+
+struct Segment {
+  bool generic;
+  uint64_t wb, we;  // word range
+  int m;
+};
+
+// Split the word range [wlo, whi) into specialised / generic segments.
+std::vector<Segment> plan(const Options& o, int s, int n, uint64_t wlo, uint64_t whi, int full_grid) {
+  std::vector<Segment> segs;
+  const int t = o.thread_bits;
+  if (!o.force_generic && n >= 5) {
+    for (int m = o.inner_bits; m >= 0; m--) {
+      const int ub = s + t + m;
+      if (ub >= 63) continue;
+      const uint64_t unit = 1ull << ub;
+      const uint64_t A = (wlo + unit - 1) & ~(unit - 1), B = whi & ~(unit - 1);
+      if (B <= A || A < wlo) continue;
+      const uint64_t O = (B - A) >> ub;
+      if (O < (uint64_t)4 * full_grid && m > 0) continue;
+      if (A > wlo) segs.push_back({true, wlo, A, 0});
+      segs.push_back({false, A, B, m});
+      if (whi > B) segs.push_back({true, B, whi, 0});
+      return segs;
+    }
+  }
+  segs.push_back({true, wlo, whi, 0});
+  return segs;
+}
+
+// Common body of count_range / eval_range.
+int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
+              cudaStream_t st, bool eval) {
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  if (p->info.max_var_id >= n)
+    return set_err(BFA_E_RANGE, "program uses x%d, needs n > %d (got n=%d)", p->info.max_var_id,
+                   p->info.max_var_id, n);
+  if (p->opt.engine != 0) return set_err(BFA_E_ARG, "engine=%d not available in this build", p->opt.engine);
+  const uint64_t full = 1ull << n;
+  if (mu_lo > mu_hi || mu_hi > full) return set_err(BFA_E_RANGE, "valuation range outside [0, 2^n)");
+  const bool whole = mu_lo == 0 && mu_hi == full;
+  const uint64_t align = eval ? 64 : 32;
+  if (!whole && ((mu_lo % align) || (mu_hi % align)))
+    return set_err(BFA_E_ARG, "range bounds must be multiples of %llu (or the whole range)",
+                   (unsigned long long)align);
+  if (eval && !out_dev) return set_err(BFA_E_ARG, "NULL output buffer");
+  if (!eval && !count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+
+  cudaError_t ce;
+  if (count_dev) {
+    ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+    if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  }
+  uint64_t wlo, whi;
+  uint32_t mask = 0xFFFFFFFFu;
+  if (n < 5) {
+    wlo = 0; whi = 1;
+    mask = (uint32_t)((1ull << (1u << n)) - 1ull);
+  } else {
+    wlo = mu_lo >> 5; whi = mu_hi >> 5;
+  }
+  if (eval && n < 6) {  // the single u64 word: high half must read 0
+    ce = cudaMemsetAsync(out_dev, 0, sizeof(uint64_t), st);
+    if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  }
+  if (whi == wlo) return BFA_OK;
+
+  const Options& o = p->opt;
+  const int T = 1 << o.thread_bits;
+  // full-chip grid estimate for planning (exact occupancy comes from the kernel)
+  const int full_grid = di.sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
+  // eval stores 2^s consecutive words per thread as one vector store: the
+  // slice's word 0 must sit at a (4 * 2^s)-byte aligned address relative to
+  // the unit grid, else use narrower slots.
+  int s_eff = o.slot_bits;
+  if (eval)
+    while (s_eff > 0 && ((reinterpret_cast<uintptr_t>(out_dev) - 4 * (uintptr_t)wlo) & ((4u << s_eff) - 1))) s_eff--;
+  std::vector<Segment> segs = plan(o, s_eff, n, wlo, whi, full_grid);
+  std::ostringstream js;
+  js << "{\"device\": " << dev << ", \"sms\": " << di.sms << ", \"segments\": [";
+  int kernels = 0;
+  uint32_t* out32 = reinterpret_cast<uint32_t*>(out_dev);
+  for (size_t k = 0; k < segs.size(); k++) {
+    const Segment& sg = segs[k];
+    bfa::KernelSpec spec;
+    spec.mode = eval ? bfa::KM_EVAL : bfa::KM_COUNT;
+    spec.generic = sg.generic;
+    spec.slot_bits = sg.generic ? 0 : s_eff;
+    spec.thread_bits = o.thread_bits;
+    spec.inner_bits = sg.generic ? 0 : sg.m;
+    spec.fuse_count = eval && count_dev != nullptr;
+    JitEntry* je = nullptr;
+    CUfunction fn;
+    rc = get_kernel(p, spec, dev, &je, &fn);
+    if (rc) return rc;
+    const int bps = o.blocks_per_sm ? o.blocks_per_sm : je->occupancy[dev];
+    const uint64_t grid_cap = (uint64_t)di.sms * bps;
+    unsigned grid;
+    uint64_t* cnt = count_dev;
+    if (sg.generic) {
+      uint64_t wb = sg.wb, wc = sg.we - sg.wb;
+      uint32_t* o32 = eval ? out32 + (sg.wb - wlo) : nullptr;
+      grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((wc + T - 1) / T, grid_cap));
+      void* args[] = {&wb, &wc, &mask, &o32, &cnt};
+      rc = launch(fn, grid, T, st, args);
+    } else {
+      const int ub = s_eff + o.thread_bits + sg.m;
+      uint64_t A = sg.wb, O = (sg.we - sg.wb) >> ub, base = wlo;
+      uint32_t* o32 = out32;
+      grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(O, grid_cap));
+      void* args[] = {&A, &O, &base, &o32, &cnt};
+      rc = launch(fn, grid, T, st, args);
+    }
+    if (rc) return rc;
+    kernels++;
+    js << (k ? ", " : "") << "{\"variant\": \"" << (sg.generic ? "generic" : "specialised") << "\", \"words\": "
+       << (sg.we - sg.wb) << ", \"s\": " << spec.slot_bits << ", \"t\": " << spec.thread_bits
+       << ", \"m\": " << spec.inner_bits << ", \"grid\": " << grid << ", \"block\": " << T
+       << ", \"regs\": " << je->regs << ", \"blocks_per_sm\": " << bps
+       << ", \"luts_thread\": " << je->stats.luts_thread << ", \"luts_outer\": " << je->stats.luts_outer
+       << ", \"luts_inner\": " << je->stats.luts_inner << ", \"words_per_iter\": " << je->stats.words_per_iter
+       << ", \"inner_vars\": " << je->stats.inner_vars << ", \"outer_vars\": " << je->stats.outer_vars
+       << ", \"thread_vars\": " << je->stats.thread_vars << "}";
+  }
+  js << "], \"kernels\": " << kernels << "}";
+  g_last_launch = js.str();
+  return BFA_OK;
+}
+
+thread_local std::map<int, uint64_t*> t_scratch;
+
+int scratch_u64(int dev, uint64_t** p) {
+  auto it = t_scratch.find(dev);
+  if (it != t_scratch.end()) { *p = it->second; return BFA_OK; }
+  uint64_t* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 64);
+  if (e != cudaSuccess) return set_err(BFA_E_NOMEM, "cudaMalloc: %s", cudaGetErrorString(e));
+  t_scratch[dev] = d;
+  *p = d;
+  return BFA_OK;
+}
+
+// Generic kernel source for `what` of bfa_dump / bfa_jit_cubin.
+int spec_for_what(const bfa_prog* p, int what, bfa::KernelSpec* spec) {
+  if (what < 1 || what > 4) return set_err(BFA_E_ARG, "what=%d", what);
+  spec->mode = what == 2 ? bfa::KM_EVAL : bfa::KM_COUNT;
+  spec->generic = what >= 3;
+  spec->materialised = what == 4;
+  spec->slot_bits = spec->generic ? 0 : p->opt.slot_bits;
+  spec->thread_bits = p->opt.thread_bits;
+  spec->inner_bits = spec->generic ? 0 : p->opt.inner_bits;
+  return BFA_OK;
+}
+
+}  // namespace
+
+// ================================================================ C ABI
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* bfa_last_error(void) { return g_err.c_str(); }
+const char* bfa_version(void) { return "bfa 0.1 (sm_100a; NVRTC static)"; }
+
+int bfa_compile(const char* expr, bfa_prog** out) {
+  if (!expr || !out) return set_err(BFA_E_ARG, "NULL argument");
+  auto p = std::make_unique<bfa_prog>();
+  std::string err;
+  if (bfa::parse_program(expr, &p->parsed, &err) != 0) return set_err(BFA_E_PARSE, "%s", err.c_str());
+  bfa_info& I = p->info;
+  const bfa::Parsed& P = p->parsed;
+  I.max_var_id = P.max_var;
+  I.tree_nodes = P.tree_nodes;
+  I.lets = P.lets;
+  I.support = (uint32_t)__builtin_popcountll(P.support_mask);
+  // G and L over the cone of the root
+  {
+    const bfa::Dag& d = P.dag;
+    std::vector<uint8_t> seen(d.nodes.size(), 0);
+    std::vector<uint32_t> st{bfa::lit_node(P.root)};
+    uint32_t g = 0;
+    uint64_t live_support = 0;
+    while (!st.empty()) {
+      uint32_t n = st.back(); st.pop_back();
+      if (seen[n]) continue;
+      seen[n] = 1;
+      const bfa::Node& nd = d.nodes[n];
+      if (nd.kind == bfa::NK_GATE) { g++; st.push_back(nd.a); st.push_back(nd.b); }
+      if (nd.kind == bfa::NK_VAR) live_support |= 1ull << nd.val;
+    }
+    I.gates = g;
+    (void)live_support;
+    I.const_value = d.nodes[bfa::lit_node(P.root)].kind == bfa::NK_CONST ? (bfa::lit_neg(P.root) ? 1 : 0) : -1;
+    uint32_t L = 0;
+    bfa::dump_ir(P, &L);
+    I.luts = L;
+  }
+  *out = p.release();
+  return BFA_OK;
+}
+
+void bfa_free(bfa_prog* p) { delete p; }
+
+int bfa_info_get(const bfa_prog* p, bfa_info* out) {
+  if (!p || !out) return set_err(BFA_E_ARG, "NULL argument");
+  *out = p->info;
+  return BFA_OK;
+}
+
+int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
+  if (!p || !key) return set_err(BFA_E_ARG, "NULL argument");
+  std::lock_guard<std::mutex> lk(p->mu);
+  std::string k(key);
+  auto bad = [&]() { return set_err(BFA_E_ARG, "option %s=%lld out of range", key, (long long)v); };
+  if (k == "slot_bits") { if (v < 0 || v > 3) return bad(); p->opt.slot_bits = (int)v; }
+  else if (k == "thread_bits") { if (v < 5 || v > 10) return bad(); p->opt.thread_bits = (int)v; }
+  else if (k == "inner_bits") { if (v < 0 || v > 8) return bad(); p->opt.inner_bits = (int)v; }
+  else if (k == "blocks_per_sm") { if (v < 0 || v > 32) return bad(); p->opt.blocks_per_sm = (int)v; }
+  else if (k == "force_generic") { if (v < 0 || v > 1) return bad(); p->opt.force_generic = (int)v; }
+  else if (k == "engine") { if (v < 0 || v > 1) return bad(); p->opt.engine = (int)v; }
+  else return set_err(BFA_E_ARG, "unknown option '%s'", key);
+  return BFA_OK;
+}
+
+int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* count_dev, void* stream) {
+  return run_range(p, n, mu_lo, mu_hi, nullptr, count_dev, (cudaStream_t)stream, false);
+}
+
+int bfa_eval_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
+                   uint64_t* count_dev, void* stream) {
+  return run_range(p, n, mu_lo, mu_hi, out_dev, count_dev, (cudaStream_t)stream, true);
+}
+
+uint64_t bfa_count(const bfa_prog* p, int n) {
+  if (n < 0 || n > 63) { set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n); return UINT64_MAX; }
+  int dev;
+  if (current_device(&dev, nullptr)) return UINT64_MAX;
+  uint64_t* d = nullptr;
+  if (scratch_u64(dev, &d)) return UINT64_MAX;
+  if (run_range(p, n, 0, 1ull << n, nullptr, d, nullptr, false)) return UINT64_MAX;
+  uint64_t h = 0;
+  cudaError_t e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) { set_err(BFA_E_CUDA, "cudaMemcpy: %s", cudaGetErrorString(e)); return UINT64_MAX; }
+  return h;
+}
+
+int bfa_eval(const bfa_prog* p, int n, uint64_t* out) {
+  if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  int rc = run_range(p, n, 0, 1ull << n, out, nullptr, nullptr, true);
+  if (rc) return rc;
+  cudaError_t e = cudaStreamSynchronize(nullptr);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "sync: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_fill_generators(int n, int n_rows, uint64_t* table_dev, void* stream) {
+  if (!table_dev || n_rows < 0) return set_err(BFA_E_ARG, "bad argument");
+  if (n < 7 || n > 40 || n_rows > n) return set_err(BFA_E_RANGE, "fill needs 7 <= n <= 40 and rows <= n");
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaError_t e = bfa_k::fill_generators(n, n_rows, table_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "fill: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_popcount(const uint64_t* vec_dev, uint64_t n_words, uint64_t* count_dev, void* stream) {
+  if (!vec_dev || !count_dev) return set_err(BFA_E_ARG, "NULL argument");
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaError_t e = bfa_k::popcount(vec_dev, n_words, count_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "popcount: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_peak_lop3(int blocks, int threads, int iters, uint32_t* sink_dev, void* stream) {
+  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !sink_dev)
+    return set_err(BFA_E_ARG, "bad argument");
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaError_t e = bfa_k::peak_lop3(blocks, threads, iters, sink_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "peak_lop3: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_eval_materialised(const bfa_prog* p, int n, int variant, uint64_t* out_dev, uint64_t* count_dev,
+                          void* stream) {
+  if (!p || !out_dev) return set_err(BFA_E_ARG, "NULL argument");
+  if (n < 7 || n > 40) return set_err(BFA_E_RANGE, "materialised mode needs 7 <= n <= 40");
+  if (p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "program uses x%d >= n", p->info.max_var_id);
+  if (variant != 0 && variant != 1) return set_err(BFA_E_ARG, "variant must be 0 or 1");
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const uint64_t words64 = 1ull << (n - 6);
+  const size_t vbytes = words64 * 8;
+  std::vector<void*> allocs;
+  auto cleanup = [&]() {
+    for (void* a : allocs) cudaFreeAsync(a, st);
+    cudaStreamSynchronize(st);
+  };
+  auto alloc = [&](void** ptr, size_t bytes) -> int {
+    cudaError_t e = cudaMallocAsync(ptr, bytes, st);
+    if (e != cudaSuccess) return set_err(BFA_E_NOMEM, "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
+    allocs.push_back(*ptr);
+    return BFA_OK;
+  };
+  const int rows = n;  // the paper's table S: n rows of 2^n bits
+  uint64_t* table = nullptr;
+  if ((rc = alloc((void**)&table, vbytes * rows))) { cleanup(); return rc; }
+  cudaError_t e = bfa_k::fill_generators(n, rows, table, st);
+  if (e != cudaSuccess) { cleanup(); return set_err(BFA_E_CUDA, "fill: %s", cudaGetErrorString(e)); }
+  std::ostringstream js;
+  int kernels = 1;
+  if (variant == 1) {
+    bfa::KernelSpec spec;
+    spec.mode = bfa::KM_EVAL;
+    spec.generic = true;
+    spec.materialised = true;
+    spec.slot_bits = 0;
+    spec.thread_bits = 8;
+    spec.inner_bits = 0;
+    spec.fuse_count = count_dev != nullptr;
+    JitEntry* je = nullptr;
+    CUfunction fn;
+    if ((rc = get_kernel(p, spec, dev, &je, &fn))) { cleanup(); return rc; }
+    if (count_dev) cudaMemsetAsync(count_dev, 0, 8, st);
+    DevInfo di;
+    current_device(&dev, &di);
+    const uint32_t* tab32 = reinterpret_cast<const uint32_t*>(table);
+    uint64_t row_words = words64 * 2, groups = words64 / 2;
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(out_dev);
+    uint64_t* cnt = count_dev;
+    unsigned grid = (unsigned)std::min<uint64_t>((groups + 255) / 256, (uint64_t)di.sms * je->occupancy[dev]);
+    void* args[] = {&tab32, &row_words, &groups, &o32, &cnt};
+    if ((rc = launch(fn, std::max(1u, grid), 256, st, args))) { cleanup(); return rc; }
+    kernels++;
+    js << "{\"variant\": \"materialised-fused\", \"luts\": " << je->stats.luts_inner << ", \"rows_loaded\": "
+       << je->stats.inner_vars << ", \"regs\": " << je->regs << ", \"grid\": " << grid;
+  } else {
+    // vector algebra: one full-vector LOP3 pass per LUT node, intermediates
+    // in a liveness-pooled set of HBM vectors.
+    bfa::Dag D;
+    std::vector<bfa::Lit> subst(64);
+    for (int v = 0; v < 64; v++) subst[v] = D.var((uint32_t)v);
+    // rebuild through the compiler's public pieces: map the unspecialised cover
+    std::string dummy;
+    bfa::Parsed const& P = p->parsed;
+    // rebuild P.root into D (identity substitution keeps the DAG as is)
+    std::vector<uint8_t> done(P.dag.nodes.size(), 0);
+    std::vector<bfa::Lit> memo(P.dag.nodes.size(), 0);
+    for (size_t k = 0; k < P.dag.nodes.size(); k++) {
+      const bfa::Node& nd = P.dag.nodes[k];
+      if (nd.kind == bfa::NK_CONST) memo[k] = k == 0 ? D.const0() : D.word(nd.val);
+      else if (nd.kind == bfa::NK_VAR) memo[k] = subst[nd.val];
+      else memo[k] = D.gate(nd.tt, memo[nd.a], memo[nd.b]);
+    }
+    bfa::Lit root = memo[bfa::lit_node(P.root)] ^ (P.root & 1u);
+    std::vector<uint8_t> lv(64, 3);
+    const double w[4] = {0, 1, 1, 1};
+    bfa::MapResult mr = bfa::map_luts(D, {root}, lv, w);
+    const bfa::Node& rn = D.nodes[bfa::lit_node(root)];
+    uint64_t logical_bytes = 0;
+    if (rn.kind == bfa::NK_CONST) {
+      cudaMemsetAsync(out_dev, bfa::lit_neg(root) ? 0xFF : 0x00, vbytes, st);
+    } else if (rn.kind == bfa::NK_VAR) {
+      const uint64_t* row = table + (uint64_t)rn.val * words64;
+      e = bfa_k::vec_lut3(out_dev, row, row, row, words64, bfa::lit_neg(root) ? 0x0F : 0xF0, st);
+      kernels++;
+      logical_bytes += 2 * vbytes;
+    } else {
+      // last use of every LUT result
+      std::map<uint32_t, size_t> pos, last;
+      for (size_t k = 0; k < mr.luts.size(); k++) pos[mr.luts[k].root] = k;
+      for (size_t k = 0; k < mr.luts.size(); k++)
+        for (int q = 0; q < mr.luts[k].nin; q++)
+          if (pos.count(mr.luts[k].in[q])) last[mr.luts[k].in[q]] = k;
+      std::vector<uint64_t*> free_list;
+      std::map<uint32_t, uint64_t*> buf;
+      size_t peak_bufs = 0;
+      for (size_t k = 0; k < mr.luts.size(); k++) {
+        const bfa::Lut& L = mr.luts[k];
+        const uint64_t* in[3];
+        for (int q = 0; q < 3; q++) {
+          const bfa::Node& nd = D.nodes[L.in[q]];
+          in[q] = nd.kind == bfa::NK_VAR ? table + (uint64_t)nd.val * words64 : buf.at(L.in[q]);
+        }
+        const bool is_out = L.root == bfa::lit_node(root);
+        uint64_t* dst;
+        if (is_out) {
+          dst = out_dev;
+        } else if (!free_list.empty()) {
+          dst = free_list.back(); free_list.pop_back();
+        } else {
+          if ((rc = alloc((void**)&dst, vbytes))) { cleanup(); return rc; }
+          peak_bufs++;
+        }
+        uint32_t imm = L.imm;
+        if (is_out && bfa::lit_neg(root)) imm ^= 0xFFu;
+        e = bfa_k::vec_lut3(dst, in[0], in[1], in[2], words64, imm, st);
+        if (e != cudaSuccess) { cleanup(); return set_err(BFA_E_CUDA, "vec_lut3: %s", cudaGetErrorString(e)); }
+        kernels++;
+        logical_bytes += (uint64_t)(L.nin + 1) * vbytes;
+        buf[L.root] = dst;
+        // release inputs whose last use was this pass
+        for (int q = 0; q < L.nin; q++) {
+          auto it = last.find(L.in[q]);
+          if (it != last.end() && it->second == k && buf.count(L.in[q])) {
+            bool dupe = false;
+            for (int r = 0; r < q; r++) dupe |= L.in[r] == L.in[q];
+            if (!dupe) free_list.push_back(buf[L.in[q]]);
+          }
+        }
+      }
+      js << "{\"variant\": \"vector-algebra\", \"passes\": " << mr.luts.size() << ", \"peak_buffers\": " << peak_bufs
+         << ", \"logical_bytes\": " << logical_bytes;
+    }
+    if (rn.kind != bfa::NK_GATE)
+      js << "{\"variant\": \"vector-algebra\", \"passes\": " << (rn.kind == bfa::NK_VAR ? 1 : 0)
+         << ", \"logical_bytes\": " << logical_bytes;
+    if (count_dev) {
+      e = bfa_k::popcount(out_dev, words64, count_dev, st);
+      kernels++;
+    }
+  }
+  js << ", \"kernels\": " << kernels << "}";
+  g_last_launch = js.str();
+  e = cudaGetLastError();
+  cleanup();
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "materialised: %s", cudaGetErrorString(e));
+  e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "materialised: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_last_launch_json(char* buf, size_t len) {
+  if (!buf || !len) return set_err(BFA_E_ARG, "NULL buffer");
+  snprintf(buf, len, "%s", g_last_launch.c_str());
+  return BFA_OK;
+}
+
+int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
+  (void)n;
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  std::string s;
+  if (what == 0) {
+    s = bfa::dump_ir(p->parsed, nullptr);
+  } else {
+    bfa::KernelSpec spec;
+    int rc = spec_for_what(p, what, &spec);
+    if (rc) return rc;
+    s = bfa::emit_kernel(p->parsed, spec, nullptr);
+  }
+  if (buf && len) snprintf(buf, len, "%s", s.c_str());
+  return (int64_t)s.size();
+}
+
+int64_t bfa_jit_cubin(const bfa_prog* p, int what, int n, void* buf, size_t len) {
+  (void)n;
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  bfa::KernelSpec spec;
+  int rc = spec_for_what(p, what, &spec);
+  if (rc) return rc;
+  JitEntry* je = nullptr;
+  rc = get_kernel(p, spec, -1, &je, nullptr);
+  if (rc) return rc;
+  if (buf && len) memcpy(buf, je->cubin.data(), std::min(len, je->cubin.size()));
+  return (int64_t)je->cubin.size();
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

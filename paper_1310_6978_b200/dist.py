@@ -1,0 +1,59 @@
+"""Cofactor sharding over GPUs.
+
+P = 2^p ranks, one process per GPU.  Rank r owns the cofactor in which the
+top p variable ids (n-1 .. n-p, the paper's b_1..b_p) spell r, i.e. the
+contiguous valuation range [r 2^(n-p), (r+1) 2^(n-p)).  Every rank runs the
+same code (no rank specialisation), so the work per rank is identical.
+
+count: the only exchange is ONE all-reduce(SUM) of the 8-byte count,
+issued on the stream that produced it (NCCL over NVLink/NVSwitch on the GPU
+box).  Counts are summed as int64; two's-complement addition is addition mod
+2^64, so the bit pattern equals the uint64 sum even at n = 63.
+eval: no collective; each rank writes its own slice of the vector.
+"""
+from __future__ import annotations
+
+
+def rank_range(n: int, rank: int, world: int):
+    """Valuation range [lo, hi) owned by `rank` of `world` (a power of two)."""
+    if world < 1 or world & (world - 1):
+        raise ValueError(f"world size {world} is not a power of two")
+    p = world.bit_length() - 1
+    if not 0 <= rank < world:
+        raise ValueError(f"rank {rank} outside [0, {world})")
+    if n - p < 5:
+        raise ValueError(f"n={n} too small to shard over {world} ranks (need n - log2(P) >= 5)")
+    span = 1 << (n - p)
+    return rank * span, (rank + 1) * span
+
+
+def count_sharded(prog, n: int, group=None, count_range=None, stream=None):
+    """Model count over all 2^n valuations, sharded over the process group.
+
+    Returns a 1-element int64 tensor holding the global count on every rank.
+    `count_range(n, lo, hi)` defaults to prog.count_range (the GPU path); the
+    CPU multi-process tests inject another range counter to exercise the
+    partition and the reduction with the gloo backend."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = rank_range(n, rank, world)
+    if count_range is None:
+        t = prog.count_range(n, lo, hi, stream=stream)
+    else:
+        t = count_range(n, lo, hi)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def eval_sharded(prog, n: int, group=None, out=None, count_out=None, stream=None):
+    """This rank's slice of the DNF vector (no collective).  Returns
+    (slice tensor, lo, hi).  Needs n - log2(P) >= 6 (whole u64 words)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = rank_range(n, rank, world)
+    if world > 1 and (hi - lo) % 64:
+        raise ValueError("sharded eval needs n - log2(P) >= 6")
+    return prog.eval_range(n, lo, hi, out=out, count_out=count_out, stream=stream), lo, hi

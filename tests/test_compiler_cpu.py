@@ -1,0 +1,156 @@
+"""CPU tests of the product's host side: the C ABI loads and exports every
+symbol include/bfa.h declares, the compiler's LUT3 cover is sound (its IR,
+interpreted here with numpy, equals the oracle's truth table), the generated
+kernels compile for sm_100a through NVRTC, and compute calls fail loudly
+without a GPU (no CPU fallback)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1310_6978_b200 as bfa
+import workloads as W
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_functions():
+    text = open(os.path.join(ROOT, "include", "bfa.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(bfa_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_abi_exports_every_declared_symbol():
+    import ctypes
+    names = header_functions()
+    assert "bfa_compile" in names and "bfa_count" in names and "bfa_eval" in names
+    lib = ctypes.CDLL(bfa.lib_path())
+    for name in names:
+        assert hasattr(lib, name), name
+    out = subprocess.run(["nm", "-D", "--defined-only", bfa.lib_path()], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (bfa_\w+)", out))
+    assert set(names) <= exported
+    # nothing but the C ABI is exported
+    assert all(s.startswith("bfa_") for s in re.findall(r" T (\S+)", out)), out
+
+
+# ----------------------------------------------------------- IR interpreter
+PAT = None
+
+
+def eval_ir(ir: str, n: int) -> np.ndarray:
+    """Interpret the LUT3 IR (bfa_dump what=0) over all 2^n valuations with
+    numpy bool arrays: lop3(a,b,c,imm) bit = imm[4a+2b+c] (PTX immLut)."""
+    mu = np.arange(1 << n, dtype=np.uint64)
+    vals = {}
+
+    def operand(tok):
+        tok = tok.strip()
+        if tok.startswith("x"):
+            return ((mu >> np.uint64(int(tok[1:]))) & np.uint64(1)).astype(bool)
+        if tok.startswith("L"):
+            return vals[tok]
+        w = int(tok, 16)
+        return np.full(1 << n, bool(w & 1))   # only 0/~0 constants can reach the IR
+    out = None
+    for line in ir.strip().splitlines():
+        lhs, rhs = [s.strip() for s in line.split("=", 1)]
+        if lhs == "out":
+            neg = rhs.startswith("~")
+            v = operand(rhs.lstrip("~"))
+            out = ~v if neg else v
+            continue
+        m = re.match(r"lop3\((.*), (.*), (.*), (0x[0-9a-f]+)\)", rhs)
+        a, b, c = (operand(m.group(k)) for k in (1, 2, 3))
+        imm = int(m.group(4), 16)
+        idx = (a.astype(np.uint8) << 2) | (b.astype(np.uint8) << 1) | c.astype(np.uint8)
+        vals[lhs] = ((imm >> idx) & 1).astype(bool)
+    return out
+
+
+@pytest.mark.parametrize("block", range(4))
+def test_lut_cover_matches_oracle_random(block):
+    for seed in range(block * 50, block * 50 + 50):
+        p = W.random_program(seed, max_n=12)
+        prog = bfa.Program(p.text)
+        info = prog.info
+        tt = eval_ir(prog.dump(0), p.n)
+        words, c = oracle.evaluate(p.text, p.n)
+        assert np.array_equal(oracle.pack_bool(tt), words), (seed, p.text)
+        if info["const_value"] >= 0:
+            assert c in (0, 1 << p.n) and c == info["const_value"] << p.n
+
+
+def test_lut_cover_matches_oracle_relations():
+    for gen, k in ((W.posets, 3), (W.posets, 4), (W.equivalences, 4), (W.linear_orders, 3),
+                   (W.bounded_posets, 4), (W.special_posets, 4)):
+        text = gen(k)
+        prog = bfa.Program(text)
+        tt = eval_ir(prog.dump(0), k * k)
+        words, _ = oracle.evaluate(text, k * k)
+        assert np.array_equal(oracle.pack_bool(tt), words)
+    text = W.random_dag(14, 300, seed=5)
+    tt = eval_ir(bfa.Program(text).dump(0), 14)
+    assert np.array_equal(oracle.pack_bool(tt), oracle.evaluate(text, 14)[0])
+
+
+def test_reduction_and_info():
+    """Reduction: constants propagate to 0/1."""
+    assert bfa.Program("x0 & ~x0").info["const_value"] == 0
+    assert bfa.Program("x3 | ~x3").info["const_value"] == 1
+    assert bfa.Program("(x1 -> 1) & (0 | 1)").info["const_value"] == 1
+    assert bfa.Program("").info["const_value"] == 1
+    i = bfa.Program("x0 & x1 | x2").info
+    assert i["const_value"] == -1 and i["gates"] == 2 and i["luts"] == 1 and i["support"] == 3
+    assert i["tree_nodes"] == 5 and i["max_var_id"] == 2
+    # hash-consing: the two antisymmetry clauses (i,j),(j,i) are one gate
+    i = bfa.Program("~x1 | ~x2\n~x2 | ~x1").info
+    assert i["gates"] == 1
+    c4 = bfa.Program(W.posets(6)).info
+    assert c4["support"] == 36 and c4["luts"] <= c4["gates"]
+
+
+@pytest.mark.parametrize("bad", ["x0 &", "(x0", "x0 x1", "2", "x63", "y", "let a = x0\nlet a = x1",
+                                 "x0 $ x1", "let = x0", "a = x0\na = x1"])
+def test_parse_errors_agree_with_oracle(bad):
+    with pytest.raises(bfa.BfaError) as e:
+        bfa.Program(bad)
+    assert e.value.code == bfa.BFA_E_PARSE
+    assert re.match(r"bfa error -1: \d+:\d+: ", str(e.value))
+
+
+def test_generated_kernels_compile_sm100a(tmp_path):
+    """Every kernel variant of a few programs JIT-compiles for sm_100a
+    (NVRTC needs no GPU); the SASS of the specialised count kernel is LOP3
+    code with no local-memory spills."""
+    for text in (W.posets(4), W.random_dag(20, 200, seed=1), "x0", "x40 ^ x7"):
+        p = bfa.Program(text)
+        for what in (1, 2, 3, 4):
+            assert len(p.jit_cubin(what)) > 1000
+    cub = tmp_path / "k.cubin"
+    cub.write_bytes(bfa.Program(W.posets(5)).jit_cubin(1))
+    sass = subprocess.run(["cuobjdump", "-sass", str(cub)], capture_output=True, text=True).stdout
+    assert "LOP3" in sass and "STL" not in sass and "LDL" not in sass
+
+
+def test_options_validation():
+    p = bfa.Program("x0")
+    with pytest.raises(bfa.BfaError):
+        p.set_option("slot_bits", 9)
+    with pytest.raises(bfa.BfaError):
+        p.set_option("nonsense", 1)
+    p.set_option("thread_bits", 7).set_option("inner_bits", 2)
+
+
+def test_no_cpu_fallback():
+    """Without a CUDA device every compute call fails loudly."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    p = bfa.Program(W.posets(3))
+    with pytest.raises(bfa.BfaError) as e:
+        p.count(9)
+    assert e.value.code == bfa.BFA_E_CUDA

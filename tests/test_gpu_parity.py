@@ -1,0 +1,258 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit
+for bit.  Vectors and counts are integer results, so the bar is exact
+equality (BASELINE.json north star: "bit-exact")."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+bfa = pytest.importorskip("paper_1310_6978_b200")
+
+
+def host(words_t):
+    return words_t.cpu().numpy().view(np.uint64)
+
+
+def check_full(text, n, prog=None):
+    prog = prog or bfa.Program(text)
+    ow, oc = oracle.evaluate(text, n)
+    gw = host(prog.eval(n))
+    assert np.array_equal(gw, ow), (text[:200], n)
+    assert prog.count(n) == oc
+    return oc
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _device():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    torch.cuda.set_device(0)
+
+
+# ------------------------------------------------------------ paper fixtures
+def test_c1_posets3(golden):
+    g = golden("c1_posets3.json")
+    p = bfa.Program(W.posets(3))
+    w = host(p.eval(9))
+    assert [int(x) for x in w] == [int(x, 16) for x in g["words_u64"]]
+    assert p.count(9) == 19
+
+
+def test_generators_and_baequ(golden):
+    g = golden("generators_n3.json")
+    for var, bits in g["vectors"].items():
+        w = host(bfa.Program(var).eval(3))
+        assert "".join(str((int(w[0]) >> mu) & 1) for mu in range(8)) == bits
+    b = golden("baequ.json")
+    w = host(bfa.Program(b["program"]).eval(4))
+    assert int(w[0]) == int(b["word0"], 16)
+
+
+@pytest.mark.parametrize("family", ["posets", "equivalences", "linear_orders", "bounded_posets",
+                                    "special_posets"])
+def test_closed_forms_gpu(golden, family):
+    g = golden("closed_forms.json")[family]
+    gen = getattr(W, family)
+    for k, expect in zip(g["k"], g["count"]):
+        if k > 5:
+            continue
+        p = bfa.Program(gen(k))
+        assert p.count(k * k) == expect, (family, k)
+
+
+def test_c3_vectors():
+    """Config C3: equivalences (52) and posets (4231) on 5 points, full
+    2^25-bit vectors against the oracle."""
+    for name in ("c3_equiv", "c3_posets"):
+        text, n, expect = W.config(name)
+        assert check_full(text, n) == expect
+
+
+# ------------------------------------------------------------ random suite
+@pytest.mark.parametrize("block", range(10))
+def test_random_terms(block):
+    """500 random terms: n = seed mod 21 in [0, 20]."""
+    for seed in range(block * 50, block * 50 + 50):
+        p = W.random_program(seed, max_n=20)
+        check_full(p.text, p.n)
+
+
+GEOMETRIES = [dict(slot_bits=0, thread_bits=5, inner_bits=0), dict(slot_bits=1, thread_bits=6, inner_bits=2),
+              dict(slot_bits=3, thread_bits=7, inner_bits=3), dict(slot_bits=2, thread_bits=8, inner_bits=4),
+              dict(force_generic=1)]
+
+
+@pytest.mark.parametrize("geo", range(len(GEOMETRIES)))
+def test_launch_geometries(geo):
+    """Results independent of the launch geometry."""
+    for seed in list(range(12, 21)) + [100, 120, 140]:
+        p = W.random_program(seed, max_n=20)
+        prog = bfa.Program(p.text)
+        for k, v in GEOMETRIES[geo].items():
+            prog.set_option(k, v)
+        check_full(p.text, p.n, prog)
+    for text, n in ((W.posets(4), 16), (W.random_dag(20, 300, seed=9), 20)):
+        prog = bfa.Program(text)
+        for k, v in GEOMETRIES[geo].items():
+            prog.set_option(k, v)
+        check_full(text, n, prog)
+
+
+def test_ranges_concatenate():
+    """P-11: range slices concatenate to the vector; range counts sum."""
+    text, n = W.random_dag(22, 400, seed=2), 22
+    p = bfa.Program(text)
+    full = host(p.eval(n))
+    total = 0
+    parts = []
+    bounds = [0, 64 * 7, 1 << 12, (1 << 20) + 64 * 3, 3 << 20, 1 << 22]
+    for lo, hi in zip(bounds, bounds[1:]):
+        parts.append(host(p.eval_range(n, lo, hi)))
+        total += int(p.count_range(n, lo, hi).item())
+    assert np.array_equal(np.concatenate(parts), full)
+    assert total == p.count(n) == oracle.count(text, n)
+    # count ranges at 32-granularity
+    lo, hi = 32 * 5, 32 * 1001
+    assert int(p.count_range(n, lo, hi).item()) == oracle.count(text, n, lo, hi)
+
+
+def test_edge_cases():
+    for n in range(0, 7):
+        check_full("1", n)
+        check_full("0", n)
+    for n in range(1, 8):
+        check_full(f"x{n - 1}", n)
+        check_full(" ^ ".join(f"x{v}" for v in range(n)), n)
+    check_full("", 5)
+    assert bfa.Program("x0 | ~x0").count(40) == 1 << 40
+    assert bfa.Program("x0 & ~x0").count(40) == 0
+    p = bfa.Program("x62 & x61 | x0")
+    lo = (1 << 63) - (1 << 20)
+    assert int(p.count_range(63, lo, 1 << 63).item()) == oracle.count("x62 & x61 | x0", 63, lo, 1 << 63)
+    with pytest.raises(bfa.BfaError) as e:
+        bfa.Program("x5").count(5)
+    assert e.value.code == bfa.BFA_E_RANGE
+    with pytest.raises(bfa.BfaError):
+        bfa.Program("x0").count(64)
+    with pytest.raises(bfa.BfaError):
+        bfa.Program("x0").count_range(20, 3, 64)
+
+
+def test_invariants_large():
+    """P-11 at sizes beyond the oracle: count(f) + count(~f) = 2^n,
+    count(f ^ x_fresh) = 2^(n-1), Shannon on one variable."""
+    text = W.random_dag(34, 500, seed=4)
+    body = "\n".join(text.splitlines()[:-1])
+    out = text.splitlines()[-1]
+    n = 34
+    c = bfa.Program(text).count(n)
+    assert c + bfa.Program(f"{body}\n~{out}").count(n) == 1 << n
+    assert bfa.Program(f"{body}\n{out} ^ x34").count(n + 1) == 1 << n
+    assert (bfa.Program(f"{body}\n{out} & x20").count(n) + bfa.Program(f"{body}\n{out} & ~x20").count(n)) == c
+
+
+# ------------------------------------------------------------ configs at full size
+def test_c4_posets6_count_and_subcubes():
+    """Config C4 at full size (n=36) in the bench launch configuration:
+    count = A001035(6) = 130023; sampled cofactor sub-cubes of the vector
+    equal the oracle's."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text)
+    assert p.count(n) == expect
+    rng = np.random.default_rng(7)
+    refl = sum(1 << (35 - 7 * i) for i in range(6))   # all p(i,i) set
+    for _ in range(3):
+        lo = (int(rng.integers(0, 1 << 36)) | refl) & ~((1 << 24) - 1)
+        hi = lo + (1 << 24)
+        ow, oc = oracle.evaluate(text, n, lo, hi)
+        gw = host(p.eval_range(n, lo, hi))
+        assert np.array_equal(gw, ow) and int(p.count_range(n, lo, hi).item()) == oc
+
+
+def test_c4_full_set_bits():
+    """P-14: the full 2^36-bit vector's set-bit list equals the oracle's
+    (full oracle run in 2^30-valuation chunks; short-circuit on the
+    reflexivity conjuncts keeps it cheap)."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text)
+    gw = p.eval(n)                               # 8 GiB on the device
+    nz = torch.nonzero(gw).flatten()
+    words = gw[nz].cpu().numpy().view(np.uint64)
+    idx = nz.cpu().numpy()
+    del gw
+    torch.cuda.empty_cache()
+    bits = np.unpackbits(words.view(np.uint8), bitorder="little").reshape(-1, 64)
+    r, c = np.nonzero(bits)
+    gbits = np.sort(idx[r].astype(np.int64) * 64 + c)
+    chunk = 1 << 30
+    obits = []
+    for k in range(1 << (n - 30)):
+        ow, _ = oracle.evaluate(text, n, k * chunk, (k + 1) * chunk)
+        obits.append(oracle.set_bits(ow, k * chunk))
+    obits = np.concatenate(obits)
+    assert len(obits) == expect == len(gbits)
+    assert np.array_equal(gbits, obits)
+
+
+def test_c5_bench_config_subcubes():
+    """Config C5 (n=42 random DAG), the bench workload, in the bench's launch
+    configuration: full count, invariant with ~f, and oracle sub-cube counts
+    (top 22 ids fixed; P-13)."""
+    text, n, _ = W.config("c5")
+    p = bfa.Program(text)
+    c = p.count(n)
+    body = "\n".join(text.splitlines()[:-1])
+    out = text.splitlines()[-1]
+    assert c + bfa.Program(f"{body}\n~{out}").count(n) == 1 << n
+    rng = np.random.default_rng(11)
+    for _ in range(4):
+        lo = int(rng.integers(0, 1 << 22)) << 20
+        hi = lo + (1 << 20)
+        assert int(p.count_range(n, lo, hi).item()) == oracle.count(text, n, lo, hi)
+        ow, _ = oracle.evaluate(text, n, lo, lo + (1 << 16))
+        assert np.array_equal(host(p.eval_range(n, lo, lo + (1 << 16))), ow)
+
+
+# ------------------------------------------------------------ materialised mode
+def test_fill_generators_and_popcount():
+    n = 12
+    tab = host(bfa.fill_generators(n)).reshape(n, -1)
+    for v in range(n):
+        ow, _ = oracle.evaluate(f"x{v}", n)
+        assert np.array_equal(tab[v], ow)
+    x = torch.randint(-(1 << 62), 1 << 62, (1001,), dtype=torch.int64, device="cuda")
+    ref = int(np.unpackbits(x.cpu().numpy().view(np.uint8)).sum())
+    assert int(bfa.popcount(x).item()) == ref
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+def test_materialised_modes(variant):
+    for text, n in ((W.cnf3(14, 30, seed=3), 14), (W.posets(4), 16), (W.random_dag(12, 150, seed=8), 12),
+                    ("x3", 9), ("~x3", 9), ("x0 & ~x0", 9)):
+        p = bfa.Program(text)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        gw = host(p.eval_materialised(n, variant, count_out=cnt))
+        ow, oc = oracle.evaluate(text, n)
+        assert np.array_equal(gw, ow), (text[:80], variant)
+        assert int(cnt.item()) == oc
+
+
+def test_c2_materialised():
+    """Config C2 (3-CNF, n=28): m=2000 gives 0 models; the m=100 variant's
+    full 2^28-bit vector equals the oracle's, in both materialised variants."""
+    text, n, expect = W.config("c2")
+    p = bfa.Program(text)
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for variant in (0, 1):
+        p.eval_materialised(n, variant, count_out=cnt)
+        assert int(cnt.item()) == expect == 0
+    text, n, _ = W.config("c2_m100")
+    ow, oc = oracle.evaluate(text, n)
+    p = bfa.Program(text)
+    for variant in (0, 1):
+        gw = host(p.eval_materialised(n, variant, count_out=cnt))
+        assert np.array_equal(gw, ow) and int(cnt.item()) == oc
+    assert p.count(n) == oc
