@@ -159,6 +159,16 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def traffic_for(cfg):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    --set full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[cfg]["dram_bytes_per_launch"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 # ---------------------------------------------------------------- GPU leg
 def measure_lop3_peak(bfa, torch, dev):
     """Measured LOP3 issue rate (reported next to the derived peak)."""
@@ -295,7 +305,7 @@ def run_bfa(args):
         "config": config_block(args.config, n, info, world),
         "count": final, "count_expected": expect,
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_derived, "unit": "LOP3/s",
-                     "frac": achieved / peak_derived, "traffic": None,
+                     "frac": achieved / peak_derived, "traffic": traffic_for(args.config),
                      "per_unit": f"{L_exec:.2f} LOP3 per 32-bit word (32 valuations) of the slot-cofactored, "
                                  f"hoisted cover ({seg['luts_inner']} inner LUTs / {S} words + "
                                  f"{seg['luts_outer']} outer LUTs / {S << m} words)",
