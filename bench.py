@@ -170,19 +170,22 @@ def traffic_for(cfg):
 
 
 # ---------------------------------------------------------------- GPU leg
-def measure_lop3_peak(bfa, torch, dev):
-    """Measured LOP3 issue rate (reported next to the derived peak)."""
+def measure_int_peaks(bfa, torch, dev):
+    """Measured integer issue rates (ops/s): LOP3 only (ALU pipe), IMAD only
+    (FMA pipe), and LOP3+IMAD 1:1 (both pipes, bounded by issue)."""
     sink = torch.zeros(4096, dtype=torch.int32, device=dev)
     blocks, threads, iters = SMS * 8, 256, 2000
-    bfa.peak_lop3(blocks, threads, 10, sink)
-    torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    bfa.peak_lop3(blocks, threads, iters, sink)
-    e.record()
-    torch.cuda.synchronize()
-    dt = s.elapsed_time(e) / 1e3
-    return blocks * threads * iters * 256 / dt
+    out = {}
+    for op, name in ((0, "lop3"), (1, "imad"), (2, "lop3_imad_1to1")):
+        bfa.peak_int(op, blocks, threads, 10, sink)
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        bfa.peak_int(op, blocks, threads, iters, sink)
+        e.record()
+        torch.cuda.synchronize()
+        out[name] = blocks * threads * iters * 256 / (s.elapsed_time(e) / 1e3)
+    return out
 
 
 def run_bfa(args):
@@ -215,7 +218,16 @@ def run_bfa(args):
         if world > 1:
             dist.all_reduce(cnt)
 
-    # JIT + warm-up (untimed)
+    # autotune (JIT of the candidate variants + probe timing; untimed), then
+    # warm-up.  Rank 0 tunes and broadcasts its choice so every rank runs the
+    # same kernel.
+    tune = prog.autotune(n) if rank == 0 else None
+    if world > 1:
+        obj = [tune]
+        dist.broadcast_object_list(obj, src=0)
+        tune = obj[0]
+    for key, val in (tune.get("best") or {}).items():
+        prog.set_option(key, val)
     for _ in range(max(args.warmup, 3)):
         step()
     torch.cuda.synchronize()
@@ -265,15 +277,21 @@ def run_bfa(args):
     L = info["luts"]
     kernel_s = t_kern / args.steps
     # Work per 32-bit word of the cover the kernel must execute: the JIT'd
-    # program is the LUT3 cover of f cofactored on the slot variables, with
-    # loop-invariant LUTs hoisted.
+    # program is the cell cover of f cofactored on the slot variables, with
+    # loop-invariant cells hoisted: LOP3 cells on the ALU pipe,
+    # IMAD cells (+ their operand registers) on the FMA pipe.
     seg = max(launch["segments"], key=lambda g: g["words"])
     S, m = seg["words_per_iter"], seg["m"]
-    L_exec = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
-    achieved = L_exec * words_per_launch / kernel_s           # LOP3/s per GPU
+    lop3_w = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
+    imad_w = (seg["imads_inner"] + seg["derived_inner"]) / S + (seg["imads_outer"] + seg["derived_outer"]) / (S << m)
+    cells_w = lop3_w + imad_w
+    achieved = cells_w * words_per_launch / kernel_s           # integer cell ops/s per GPU
     sm_clock = clk["sm_max_mhz"] or 1965.0
-    peak_derived = SMS * LOP3_PER_CLK_PER_SM * sm_clock * 1e6
-    peak_measured = measure_lop3_peak(bfa, torch, dev)
+    # derived: the scheduler issues 1 warp-instruction/clk per SMSP; LOP3 takes
+    # the ALU pipe (16 lanes/clk/SMSP), IMAD the FMA pipe (32 lanes/clk/SMSP)
+    peak_issue = SMS * 4 * 32 * sm_clock * 1e6
+    peak_alu = SMS * LOP3_PER_CLK_PER_SM * sm_clock * 1e6
+    peaks = measure_int_peaks(bfa, torch, dev)
 
     # e2e: the public C-ABI call with a host result (bfa_count -> uint64 on the
     # host: launch + 8-byte D2H + sync every step).  Count mode has no input
@@ -304,23 +322,26 @@ def run_bfa(args):
         "data": "synthetic (seeded generator, workloads/__init__.py)",
         "config": config_block(args.config, n, info, world),
         "count": final, "count_expected": expect,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peak_derived, "unit": "LOP3/s",
-                     "frac": achieved / peak_derived, "traffic": traffic_for(args.config),
-                     "per_unit": f"{L_exec:.2f} LOP3 per 32-bit word (32 valuations) of the slot-cofactored, "
-                                 f"hoisted cover ({seg['luts_inner']} inner LUTs / {S} words + "
-                                 f"{seg['luts_outer']} outer LUTs / {S << m} words)",
-                     "nominal_L": L, "nominal_frac": L * words_per_launch / kernel_s / peak_derived,
+        "roofline": {"bound": "alu", "achieved": achieved, "peak": peaks["lop3_imad_1to1"], "unit": "int ops/s",
+                     "frac": achieved / peaks["lop3_imad_1to1"], "traffic": traffic_for(args.config),
+                     "per_unit": f"{cells_w:.2f} integer cells per 32-bit word (32 valuations): {lop3_w:.2f} LOP3 "
+                                 f"+ {imad_w:.2f} IMAD of the slot-cofactored, hoisted cover",
                      "units_per_launch": words_per_launch,
-                     "peak_source": f"derived: {SMS} SMs x {LOP3_PER_CLK_PER_SM} LOP3/clk/SM x {sm_clock:.0f} MHz "
-                                    "(B300_MICROARCH.md alu-pipe rate; sm_max clock)",
-                     "peak_measured_lop3": peak_measured, "frac_of_measured": achieved / peak_measured,
-                     "gate_word_ops_per_s": info["gates"] * words_per_launch / kernel_s},
+                     "peak_source": "measured bfa_peak_int LOP3+IMAD 1:1 (issue-bound: 1 warp-inst/clk/SMSP)",
+                     "peak_derived_issue": peak_issue, "frac_of_derived_issue": achieved / peak_issue,
+                     "peak_measured": peaks,
+                     "alu_pipe": {"lop3_per_s": lop3_w * words_per_launch / kernel_s, "peak_derived": peak_alu,
+                                  "frac": lop3_w * words_per_launch / kernel_s / peaks["lop3"]},
+                     "nominal": {"L": L, "G": info["gates"],
+                                 "lop3_equiv_per_s": L * words_per_launch / kernel_s,
+                                 "gate_word_ops_per_s": info["gates"] * words_per_launch / kernel_s}},
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
                 "call": "bfa_count(prog, n) -> host uint64"},
         "gpu_launches": kernels_per_step * args.steps,
         "kernel_ms_per_step": kernel_s * 1e3,
         "launch": launch,
+        "autotune": tune,
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -91,15 +91,29 @@ void bfa_free(bfa_prog* p);                                 /* NULL-safe */
 int bfa_info_get(const bfa_prog* p, bfa_info* out);
 
 /* Launch options (part of the JIT cache key).  Keys:
- *   "slot_bits"     log2 words per thread per iteration, 0..3   (default 2)
+ *   "slot_bits"     log2 words per thread per iteration, 0..5   (default 2)
  *   "thread_bits"   log2 threads per block, 5..10               (default 8)
  *   "inner_bits"    max log2 inner-loop trip count, 0..8        (default 4)
  *   "blocks_per_sm" resident blocks per SM targeted, 0 = occupancy API (default 0)
  *   "force_generic" 1 = always use the unspecialised word-per-thread kernel
  *   "engine"        0 = JIT straight-line LOP3 (default), 1 = constant-memory
  *                   interpreter (ablation)
+ *   "dual_pipe"     1 = map gates with a word-uniform input to IMAD cells on the
+ *                   FMA pipe next to LOP3 cells on the ALU pipe (default 1)
+ *   "imad_cost_pct" IMAD:LOP3 cost ratio in percent for that mapping, 0 = model
+ *                   sweep (default 0)
+ *   "min_blocks"    __launch_bounds__ minimum blocks per SM, 0 = none (default 0)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
+
+/* Empirical autotuning of the register-mode kernel for n variables: JIT
+ * compiles a set of candidate variants (slot bits, inner-loop bits, IMAD/LOP3
+ * balance) in parallel, times each on the top min(2^n, 2^36) valuations with
+ * CUDA events on `stream`, and sets p's options to the fastest.  Writes a JSON
+ * report (candidates, times, choice) to report (nullable).  Results do not
+ * depend on the options; only speed does.  Not thread-safe with other calls on
+ * the same program.  n < 24: no-op. */
+int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len);
 
 /* ---- register-synthesised mode (generators built in registers) ---- */
 
@@ -146,10 +160,12 @@ int bfa_popcount(const uint64_t* vec_dev, uint64_t n_words, uint64_t* count_dev,
 
 /* ---- measurement ---- */
 
-/* LOP3 throughput microbenchmark: launches blocks x threads threads, each
- * executing `iters` x 256 dependent-free lop3.b32 (8 independent chains).
- * The caller times it; ops = blocks * threads * iters * 256. */
-int bfa_peak_lop3(int blocks, int threads, int iters, uint32_t* sink_dev, void* stream);
+/* Integer issue-rate microbenchmark (the roofline denominators): launches
+ * blocks x threads (<= 256) threads, each executing iters x 256 operations in
+ * 8 independent chains.  op 0: lop3.b32 (ALU pipe), 1: mad.lo.u32 (IMAD, FMA
+ * pipe), 2: both, interleaved 1:1.  The caller times it with events;
+ * ops = blocks * threads * iters * 256. */
+int bfa_peak_int(int op, int blocks, int threads, int iters, uint32_t* sink_dev, void* stream);
 
 /* Statistics of the kernel variant the last launch on this thread used:
  * executed LUTs per 32-bit word at each loop level etc., as a JSON object

@@ -14,7 +14,7 @@ import json
 import os
 
 __all__ = ["Program", "BfaError", "words_for", "last_launch", "fill_generators", "popcount",
-           "peak_lop3", "lib_path", "version"]
+           "peak_int", "lib_path", "version"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbfa.so")
@@ -37,10 +37,11 @@ _SIGS = {
     "bfa_fill_generators": (_c.c_int, [_c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
     "bfa_eval_materialised": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p, _c.c_void_p]),
     "bfa_popcount": (_c.c_int, [_c.c_void_p, _c.c_uint64, _c.c_void_p, _c.c_void_p]),
-    "bfa_peak_lop3": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
+    "bfa_peak_int": (_c.c_int, [_c.c_int, _c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
     "bfa_last_launch_json": (_c.c_int, [_c.c_char_p, _c.c_size_t]),
     "bfa_dump": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t]),
     "bfa_jit_cubin": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_size_t]),
+    "bfa_autotune": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_char_p, _c.c_size_t]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -141,6 +142,12 @@ class Program:
         _check(_load().bfa_set_option(self._h, key.encode(), int(value)))
         return self
 
+    def autotune(self, n: int, stream=None) -> dict:
+        """bfa_autotune: pick the fastest kernel variant for n (sets options)."""
+        buf = ctypes.create_string_buffer(1 << 16)
+        _check(_load().bfa_autotune(self._h, n, _stream(stream), buf, len(buf)))
+        return json.loads(buf.value.decode())
+
     # ---- register-synthesised mode
     def count(self, n: int) -> int:
         """bfa_count: number of models over all 2^n valuations (synchronous)."""
@@ -216,5 +223,6 @@ def popcount(vec, count_out=None, stream=None):
     return count_out
 
 
-def peak_lop3(blocks: int, threads: int, iters: int, sink, stream=None):
-    _check(_load().bfa_peak_lop3(blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream(stream)))
+def peak_int(op: int, blocks: int, threads: int, iters: int, sink, stream=None):
+    """bfa_peak_int: op 0 LOP3, 1 IMAD, 2 LOP3+IMAD 1:1; 256 ops/thread/iter."""
+    _check(_load().bfa_peak_int(op, blocks, threads, iters, ctypes.c_void_p(sink.data_ptr()), _stream(stream)))

@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <set>
 #include <sstream>
 
 namespace bfa {
@@ -400,8 +402,21 @@ inline uint8_t expand(const Cut& c, const uint32_t* L, int nl) {
 
 }  // namespace
 
+// IMAD option of a gate (x, u, f0, f1); valid when u is word-uniform
+struct ImadOpt {
+  uint32_t x = 0, u = 0;
+  uint8_t f0 = 0, f1 = 0;
+  bool ok = false;
+};
+
+// unary code of f over x from (f(0), f(1)): 0:"0" 1:"~0" 2:"x" 3:"~x"
+static inline uint8_t unary_code(int v0, int v1) {
+  if (v0 == v1) return v0 ? 1 : 0;
+  return v1 ? 2 : 3;
+}
+
 MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
-                   const std::vector<uint8_t>& var_level, const double weights[4]) {
+                   const std::vector<uint8_t>& var_level, const double weights[4], double imad_cost) {
   const size_t N = dag.nodes.size();
   MapResult res;
   res.node_level.assign(N, 0);
@@ -426,6 +441,16 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
     if (nd.kind == NK_VAR) res.node_level[n] = var_level[nd.val];
     else if (nd.kind == NK_GATE) res.node_level[n] = std::max(res.node_level[nd.a], res.node_level[nd.b]);
   }
+  // word-uniform nodes: 0 or ~0 in every 32-bit word (no lane mask in the cone)
+  std::vector<uint8_t> uniform(N, 0);
+  for (size_t n = 0; n < N; n++) {
+    const Node& nd = dag.nodes[n];
+    if (nd.kind == NK_VAR) uniform[n] = 1;
+    else if (nd.kind == NK_CONST) uniform[n] = n == 0;
+    else uniform[n] = uniform[nd.a] && uniform[nd.b];
+  }
+  std::vector<ImadOpt> imad(N);
+  std::vector<uint8_t> use_imad(N, 0);
   const int kMaxCuts = 8;
   std::vector<std::vector<Cut>> cuts(N);
   std::vector<float> af(N, 0.f);
@@ -473,6 +498,26 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
     });
     if ((int)cand.size() > kMaxCuts) cand.resize(kMaxCuts);
     af[n] = cand.empty() ? (float)weights[res.node_level[n]] : cand[0].cost;
+    // IMAD cell: u ? f1(x) : f0(x) for a word-uniform input u
+    if (imad_cost > 0 && (uniform[nd.a] || uniform[nd.b])) {
+      ImadOpt o;
+      // prefer as u the uniform input at the lower loop level (its operand
+      // registers are computed less often); tie -> input b
+      bool ub = uniform[nd.b] && (!uniform[nd.a] || res.node_level[nd.b] <= res.node_level[nd.a]);
+      if (ub) {   // tt bit (a + 2b): x = a, u = b
+        o.x = nd.a; o.u = nd.b;
+        o.f0 = unary_code(nd.tt & 1, (nd.tt >> 1) & 1);
+        o.f1 = unary_code((nd.tt >> 2) & 1, (nd.tt >> 3) & 1);
+      } else {    // x = b, u = a
+        o.x = nd.b; o.u = nd.a;
+        o.f0 = unary_code(nd.tt & 1, (nd.tt >> 2) & 1);
+        o.f1 = unary_code((nd.tt >> 1) & 1, (nd.tt >> 3) & 1);
+      }
+      o.ok = true;
+      imad[n] = o;
+      float c = (float)(weights[res.node_level[n]] * imad_cost) + leaf_share(o.x) + leaf_share(o.u);
+      if (c < af[n]) { af[n] = c; use_imad[n] = 1; }
+    }
     cuts[n] = cand;
     cuts[n].push_back(triv);
   }
@@ -481,6 +526,19 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
   for (Lit o : outputs) req[lit_node(o)] = 1;
   for (size_t k = N; k-- > 0;) {
     if (!req[k] || dag.nodes[k].kind != NK_GATE) continue;
+    if (use_imad[k]) {
+      const ImadOpt& o = imad[k];
+      Lut cell{};
+      cell.root = (uint32_t)k;
+      cell.kind = 1;
+      cell.nin = 2;
+      cell.in[0] = o.x; cell.in[1] = o.u; cell.in[2] = o.u;
+      cell.f0 = o.f0; cell.f1 = o.f1;
+      cell.level = res.node_level[k];
+      res.luts.push_back(cell);
+      req[o.x] = 1; req[o.u] = 1;
+      continue;
+    }
     const Cut& c = cuts[k][0];
     Lut lut{};
     lut.root = (uint32_t)k;
@@ -526,12 +584,77 @@ struct Emitter {
     if (nd.kind == NK_CONST) return hex32(lit_neg(l) ? ~nd.val : nd.val);
     return lit_neg(l) ? "(~" + name(lit_node(l)) + ")" : name(lit_node(l));
   }
+  // IMAD operand registers: (u, k, c) -> u * k + c, computed once at u's level
+  std::map<uint32_t, std::set<std::pair<int, int>>> derived;
+
+  static void mc(uint8_t f, int* m, int* c) {  // unary f(x) = x * m + c
+    switch (f) {
+      case 0: *m = 0; *c = 0; break;    // 0
+      case 1: *m = 0; *c = -1; break;   // ~0
+      case 2: *m = 1; *c = 0; break;    // x
+      default: *m = -1; *c = -1; break; // ~x
+    }
+  }
+  static std::string dname(uint32_t u, int k, int c) {
+    auto enc = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    return "d" + std::to_string(u) + "_" + enc(k) + "_" + enc(c);
+  }
+  static std::string imm(int v) {
+    char b[16];
+    snprintf(b, sizeof b, "0x%08xu", (uint32_t)v);
+    return b;
+  }
+  // operand of an affine function of u: k*u + c
+  std::string affine(uint32_t u, int k, int c, bool record) {
+    if (k == 0) return "\"n\"(" + imm(c) + ")";
+    if (k == 1 && c == 0) return "\"r\"(" + name(u) + ")";
+    if (record) derived[u].insert({k, c});
+    return "\"r\"(" + dname(u, k, c) + ")";
+  }
+  // register the operand registers an IMAD cell needs (before emission)
+  void plan_cell(const Lut& L) {
+    if (L.kind != 1) return;
+    int m0, c0, m1, c1;
+    mc(L.f0, &m0, &c0);
+    mc(L.f1, &m1, &c1);
+    if (d.nodes[L.in[0]].kind == NK_CONST) return;
+    affine(L.in[1], m0 - m1, m0, true);
+    affine(L.in[1], c0 - c1, c0, true);
+  }
+  void emit_derived(uint32_t u, const char* indent) {
+    auto it = derived.find(u);
+    if (it == derived.end()) return;
+    for (auto& kc : it->second)
+      os << indent << "const u32 " << dname(u, kc.first, kc.second) << " = " << name(u) << " * " << imm(kc.first)
+         << " + " << imm(kc.second) << ";\n";
+  }
   void lut(const Lut& L, const char* indent) {
-    char imm[8];
-    snprintf(imm, sizeof imm, "0x%02x", L.imm);
-    os << indent << "u32 " << name(L.root) << "; asm(\"lop3.b32 %0, %1, %2, %3, " << imm
-       << ";\" : \"=r\"(" << name(L.root) << ") : " << operand(L.in[0]) << ", " << operand(L.in[1])
-       << ", " << operand(L.in[2]) << ");\n";
+    if (L.kind == 1) {
+      // u ? f1(x) : f0(x) = x * M + C with M = m0 + (m0 - m1) u, C = c0 + (c0 - c1) u
+      // (u is 0 or ~0 = -1 in every word)
+      int m0, c0, m1, c1;
+      mc(L.f0, &m0, &c0);
+      mc(L.f1, &m1, &c1);
+      const Node& xn = d.nodes[L.in[0]];
+      if (xn.kind == NK_CONST) {  // constant x: K0 + (K0 - K1) u
+        uint32_t K = xn.val;
+        uint32_t K0 = (uint32_t)((int)K * m0 + c0), K1 = (uint32_t)((int)K * m1 + c1);
+        os << indent << "u32 " << name(L.root) << "; asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(" << name(L.root)
+           << ") : \"r\"(" << name(L.in[1]) << "), \"n\"(" << imm((int)(K0 - K1)) << "), \"n\"(" << imm((int)K0)
+           << "));\n";
+      } else {
+        os << indent << "u32 " << name(L.root) << "; asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(" << name(L.root)
+           << ") : \"r\"(" << name(L.in[0]) << "), " << affine(L.in[1], m0 - m1, m0, false) << ", "
+           << affine(L.in[1], c0 - c1, c0, false) << ");\n";
+      }
+    } else {
+      char immb[8];
+      snprintf(immb, sizeof immb, "0x%02x", L.imm);
+      os << indent << "u32 " << name(L.root) << "; asm(\"lop3.b32 %0, %1, %2, %3, " << immb
+         << ";\" : \"=r\"(" << name(L.root) << ") : " << operand(L.in[0]) << ", " << operand(L.in[1])
+         << ", " << operand(L.in[2]) << ");\n";
+    }
+    emit_derived(L.root, indent);
   }
 };
 
@@ -601,26 +724,77 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   for (int v = 0; v < 64; v++) var_level[v] = (uint8_t)level_of(v);
   const double iters_inner = (double)(1u << m);
   const double w[4] = {0.0, 1e-4, spec.generic ? 1.0 : 1.0 / iters_inner, 1.0};
-  MapResult mr = map_luts(D, outs, var_level, w);
 
-  // which variables are referenced (as LUT inputs or outputs)
+  // Technology mapping.  With dual_pipe, gates that have a word-uniform input
+  // may become IMAD cells (FMA pipe) instead of being absorbed into LOP3 cells
+  // (ALU pipe); sweep the IMAD:LOP3 cost ratio and keep the cover minimising
+  // the modelled time per thread-iteration, max(2 A, F, A + F + other): the
+  // ALU pipe takes a LOP3 warp-instruction every 2 cycles per SMSP, the FMA
+  // pipe an IMAD every cycle (measured with bfa_peak_int), and the scheduler
+  // issues one instruction per cycle.
+  auto model = [&](const MapResult& r, double* A_out, double* F_out) {
+    double A = 0, F = 0;
+    Emitter probe(D, os);
+    for (const Lut& L : r.luts) {
+      if (L.kind == 1) { F += w[L.level]; probe.plan_cell(L); }
+      else A += w[L.level];
+    }
+    std::vector<uint8_t> lvl = r.node_level;
+    for (auto& kv : probe.derived) F += w[lvl[kv.first]] * (double)kv.second.size();
+    const double other = spec.generic ? 4.0 : S + S / 2.0 + 2.0 + 2.0 * m;
+    if (A_out) *A_out = A;
+    if (F_out) *F_out = F;
+    return std::max({2 * (A + other), F, A + F + other});
+  };
+  MapResult mr = map_luts(D, outs, var_level, w, 0.0);
+  double best = model(mr, nullptr, nullptr);
+  st.imad_cost = 0.0;
+  if (spec.dual_pipe && !spec.materialised) {
+    std::vector<double> sweep = {0.6, 0.75, 0.9, 1.0, 1.15, 1.3, 1.6, 2.0, 3.0};
+    if (spec.imad_cost_pct > 0) { sweep = {spec.imad_cost_pct / 100.0}; best = 1e300; }
+    for (double c : sweep) {
+      MapResult r = map_luts(D, outs, var_level, w, c);
+      double tm = model(r, nullptr, nullptr);
+      if (tm < best - 1e-9) { best = tm; mr = std::move(r); st.imad_cost = c; }
+    }
+  }
+
+  // which variables are referenced (as cell inputs or outputs)
   std::vector<uint8_t> used(64, 0);
+  std::vector<uint32_t> var_node(64, 0);
+  for (size_t k = 0; k < D.nodes.size(); k++)
+    if (D.nodes[k].kind == NK_VAR) var_node[D.nodes[k].val] = (uint32_t)k;
   auto mark = [&](uint32_t n) { if (D.nodes[n].kind == NK_VAR) used[D.nodes[n].val] = 1; };
   for (const Lut& L : mr.luts) for (int q = 0; q < 3; q++) mark(L.in[q]);
   for (Lit o : outs) mark(lit_node(o));
 
+  const std::string bounds = std::to_string(1 << t) + (spec.min_blocks > 0 ? ", " + std::to_string(spec.min_blocks) : "");
   Emitter E(D, os);
+  for (const Lut& L : mr.luts) E.plan_cell(L);
+  for (auto& kv : E.derived) {
+    int lv = mr.node_level[kv.first];
+    if (lv == 3) st.derived_inner += (uint32_t)kv.second.size();
+    if (lv == 2) st.derived_outer += (uint32_t)kv.second.size();
+  }
   auto emit_level = [&](int lvl, const char* ind) {
-    uint32_t c = 0;
-    for (const Lut& L : mr.luts) if (L.level == lvl) { E.lut(L, ind); c++; }
-    return c;
+    for (const Lut& L : mr.luts) {
+      if (L.level != lvl) continue;
+      E.lut(L, ind);
+      uint32_t* luts = lvl == 1 ? &st.luts_thread : lvl == 2 ? &st.luts_outer : &st.luts_inner;
+      uint32_t* imads = lvl == 1 ? &st.imads_thread : lvl == 2 ? &st.imads_outer : &st.imads_inner;
+      (*(L.kind == 1 ? imads : luts))++;
+    }
+  };
+  auto declare_var = [&](int v, const std::string& expr, const char* ind) {
+    os << ind << "const u32 v" << v << " = " << expr << ";\n";
+    E.emit_derived(var_node[v], ind);
   };
 
   if (spec.generic && spec.materialised) {
     // the paper's table S in HBM: 128-bit loads of every
     // generator row the program uses, the LOP3 body in registers, 128-bit store
     os << "__device__ __forceinline__ u32 comp(const uint4& v, int c) { return c == 0 ? v.x : c == 1 ? v.y : c == 2 ? v.z : v.w; }\n"
-       << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+       << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
        << "bfa_kernel(const u32* __restrict__ table, const u64 row_words, const u64 groups, u32* __restrict__ out, u64* __restrict__ count) {\n"
        << "  u64 acc = 0;\n"
        << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
@@ -633,9 +807,8 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
        << "    #pragma unroll\n"
        << "    for (int c = 0; c < 4; ++c) {\n";
     for (int v = 0; v < 64; v++)
-      if (used[v]) os << "      const u32 v" << v << " = comp(V" << v << ", c);\n";
-    for (const Lut& L : mr.luts) E.lut(L, "      ");
-    st.luts_inner = (uint32_t)mr.luts.size();
+      if (used[v]) declare_var(v, "comp(V" + std::to_string(v) + ", c)", "      ");
+    emit_level(3, "      ");
     os << "      R[c] = " << E.value(outs[0]) << ";\n"
        << "    }\n";
     if (spec.mode == KM_EVAL)
@@ -647,16 +820,15 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     st.words_per_iter = 4;
     for (int v = 0; v < 64; v++) st.inner_vars += used[v];
   } else if (spec.generic) {
-    os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+    os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
        << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ out, u64* __restrict__ count) {\n"
        << "  u64 acc = 0;\n"
        << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
        << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += stride) {\n"
        << "    const u64 w = w_begin + k;\n";
     for (int v = 5; v < 64; v++)
-      if (used[v]) os << "    const u32 v" << v << " = 0u - (u32)((w >> " << (v - 5) << ") & 1ull);\n";
-    for (const Lut& L : mr.luts) E.lut(L, "    ");
-    st.luts_inner = (uint32_t)mr.luts.size();
+      if (used[v]) declare_var(v, "0u - (u32)((w >> " + std::to_string(v - 5) + ") & 1ull)", "    ");
+    emit_level(3, "    ");
     os << "    const u32 r = (" << E.value(outs[0]) << ") & mask;\n";
     if (spec.mode == KM_EVAL) os << "    out[k] = r;\n";
     if (want_count) os << "    acc += __popc(r);\n";
@@ -667,7 +839,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     for (int v = 5; v < 64; v++) st.inner_vars += used[v];
   } else {
     const int unit = s + t + m;
-    os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << t) << ")\n"
+    os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
        << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count) {\n"
        << "  const u32 tid = threadIdx.x;\n"
        << "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n"
@@ -675,29 +847,29 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
        << "  const u64 o_end = o_begin + q + (b < rr ? 1ull : 0ull);\n";
     for (int v = 5; v < 64; v++)
       if (used[v] && level_of(v) == 1) {
-        os << "  const u32 v" << v << " = 0u - ((tid >> " << (v - 5 - s) << ") & 1u);\n";
+        declare_var(v, "0u - ((tid >> " + std::to_string(v - 5 - s) + ") & 1u)", "  ");
         st.thread_vars++;
       }
-    st.luts_thread = emit_level(1, "  ");
+    emit_level(1, "  ");
     os << "  u64 acc = 0;\n"
        << "  for (u64 o = o_begin; o < o_end; ++o) {\n"
        << "    const u64 wo = A + (o << " << unit << ");\n";
     for (int v = 5; v < 64; v++)
       if (used[v] && level_of(v) == 2) {
-        os << "    const u32 v" << v << " = 0u - (u32)((wo >> " << (v - 5) << ") & 1ull);\n";
+        declare_var(v, "0u - (u32)((wo >> " + std::to_string(v - 5) + ") & 1ull)", "    ");
         st.outer_vars++;
       }
-    st.luts_outer = emit_level(2, "    ");
+    emit_level(2, "    ");
     os << "    u32 acc32 = 0;\n"
        << "    #pragma unroll 1\n"
        << "    for (u32 i = 0; i < " << (1u << m) << "u; ++i) {\n";
     for (int v = 5; v < 64; v++)
       if (used[v] && level_of(v) == 3) {
         int k = v - 5 - s - t;
-        os << "      const u32 v" << v << " = (u32)(((int)(i << " << (31 - k) << ")) >> 31);\n";
+        declare_var(v, "(u32)(((int)(i << " + std::to_string(31 - k) + ")) >> 31)", "      ");
         st.inner_vars++;
       }
-    st.luts_inner = emit_level(3, "      ");
+    emit_level(3, "      ");
     for (int sl = 0; sl < S; sl++) os << "      const u32 r" << sl << " = " << E.value(outs[sl]) << ";\n";
     if (spec.mode == KM_EVAL) {
       os << "      const u64 idx = (wo - out_base_w) + ((u64)i << " << (s + t) << ") + ((u64)tid << " << s << ");\n";

@@ -85,6 +85,11 @@ struct Lut {
   uint32_t in[3];     // leaf node ids (VAR, CONST or GATE roots)
   uint8_t imm;        // lop3 immLut over (in[0], in[1], in[2]) ~ (0xF0, 0xCC, 0xAA)
   uint8_t level;      // loop level of the root
+  // kind 1 = IMAD cell (FMA pipe): root = u ? f1(x) : f0(x) with x = in[0] and
+  // u = in[1] a word-uniform value (0 or ~0 in every word); f0/f1 are unary
+  // codes 0:"0", 1:"~0", 2:"x", 3:"~x"; emitted as x * M(u) + C(u).
+  uint8_t kind = 0;
+  uint8_t f0 = 0, f1 = 0;
 };
 
 // Map the DAG (restricted to the cones of `outputs`) onto 3-input LUTs.
@@ -94,8 +99,11 @@ struct MapResult {
   std::vector<Lut> luts;                 // topological order
   std::vector<uint8_t> node_level;       // per node of the dag
 };
+// imad_cost > 0 enables IMAD cells for gates with a word-uniform input, at
+// that cost relative to one LUT (two-resource area flow).
 MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
-                   const std::vector<uint8_t>& var_level, const double weights[4]);
+                   const std::vector<uint8_t>& var_level, const double weights[4],
+                   double imad_cost = 0.0);
 
 // ---------------------------------------------------------------- kernels
 enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1 };
@@ -109,10 +117,16 @@ struct KernelSpec {
   bool fuse_count = false;  // eval mode: also popcount
   bool materialised = false;  // generic only: every generator word is LOADED from the
                               // table S (128-bit loads, 4 words per thread-iteration)
+  int dual_pipe = 1;          // 1: balance LOP3 (ALU pipe) and IMAD (FMA pipe) cells
+  int imad_cost_pct = 0;      // >0: fixed IMAD:LOP3 cost ratio (percent) instead of the sweep
+  int min_blocks = 0;         // >0: __launch_bounds__ minimum resident blocks per SM
 };
 
 struct KernelStats {
-  uint32_t luts_thread = 0, luts_outer = 0, luts_inner = 0;  // LUTs emitted per level
+  uint32_t luts_thread = 0, luts_outer = 0, luts_inner = 0;  // LOP3 cells emitted per level
+  uint32_t imads_thread = 0, imads_outer = 0, imads_inner = 0;  // IMAD cells per level
+  uint32_t derived_inner = 0, derived_outer = 0;  // IMAD operand registers computed per level
+  double imad_cost = 0.0;                         // the mapping's chosen IMAD/LUT cost ratio
   uint32_t inner_vars = 0, outer_vars = 0, thread_vars = 0;
   uint32_t words_per_iter = 1;
 };

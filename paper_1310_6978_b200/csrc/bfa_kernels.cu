@@ -123,6 +123,46 @@ __global__ void __launch_bounds__(256) peak_lop3_kernel(u32* sink, int iters, u3
   if (acc == 0x12345678u) sink[blockIdx.x] = acc;  // keep the chains alive
 }
 
+// IMAD-only and LOP3+IMAD 1:1 variants of the issue-rate microbenchmark
+__global__ void __launch_bounds__(256) peak_imad_kernel(u32* sink, int iters, u32 seed) {
+  u32 x[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) x[j] = seed ^ (threadIdx.x * 0x9E3779B9u) ^ (j * 0x85EBCA6Bu);
+  const u32 y = seed * 3u + blockIdx.x, z = seed ^ 0x5bd1e995u;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+#pragma unroll
+      for (int j = 0; j < 8; j++) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[j]) : "r"(y), "r"(z));
+    }
+  }
+  u32 acc = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) acc ^= x[j];
+  if (acc == 0x12345678u) sink[blockIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(256) peak_mix_kernel(u32* sink, int iters, u32 seed) {
+  u32 x[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) x[j] = seed ^ (threadIdx.x * 0x9E3779B9u) ^ (j * 0x85EBCA6Bu);
+  const u32 y = seed * 3u + blockIdx.x, z = seed ^ 0x5bd1e995u;
+  for (int it = 0; it < iters; it++) {
+#pragma unroll
+    for (int r = 0; r < 32; r++) {
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(x[j]) : "r"(y), "r"(z));
+        asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(x[j + 1]) : "r"(y), "r"(z));
+      }
+    }
+  }
+  u32 acc = 0;
+#pragma unroll
+  for (int j = 0; j < 8; j++) acc ^= x[j];
+  if (acc == 0x12345678u) sink[blockIdx.x] = acc;
+}
+
 int grid_for(u64 items, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -164,8 +204,10 @@ cudaError_t popcount(const uint64_t* v, uint64_t n_words, uint64_t* count, cudaS
   return cudaGetLastError();
 }
 
-cudaError_t peak_lop3(int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st) {
-  peak_lop3_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
+cudaError_t peak_int(int op, int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st) {
+  if (op == 0) peak_lop3_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
+  else if (op == 1) peak_imad_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
+  else peak_mix_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
   return cudaGetLastError();
 }
 

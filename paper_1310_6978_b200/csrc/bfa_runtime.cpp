@@ -25,6 +25,7 @@
 #include <mutex>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/bfa.h"
@@ -147,6 +148,9 @@ struct Options {
   int blocks_per_sm = 0;
   int force_generic = 0;
   int engine = 0;
+  int dual_pipe = 1;
+  int imad_cost_pct = 0;
+  int min_blocks = 0;
 };
 
 struct JitEntry {
@@ -173,25 +177,33 @@ namespace {
 std::string spec_key(const bfa::KernelSpec& s) {
   std::ostringstream k;
   k << s.mode << (s.generic ? 'g' : 's') << s.slot_bits << '.' << s.thread_bits << '.' << s.inner_bits
-    << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-');
+    << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-') << 'd' << s.dual_pipe << '.' << s.imad_cost_pct << 'b' << s.min_blocks;
   return k.str();
 }
 
 // Compile (once) the variant `spec` of p; if dev >= 0 also load it on dev.
+// NVRTC runs outside the program lock, so candidates compile in parallel.
 int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntry** out, CUfunction* fn) {
   bfa_prog* p = const_cast<bfa_prog*>(cp);
-  std::lock_guard<std::mutex> lk(p->mu);
-  std::string key = spec_key(spec);
-  auto it = p->jit.find(key);
-  if (it == p->jit.end()) {
-    auto e = std::make_unique<JitEntry>();
-    e->source = bfa::emit_kernel(p->parsed, spec, &e->stats);
-    int rc = nvrtc_compile(e->source, &e->cubin);
-    if (rc) return rc;
-    it = p->jit.emplace(key, std::move(e)).first;
+  const std::string key = spec_key(spec);
+  JitEntry* e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->jit.find(key);
+    if (it != p->jit.end()) e = it->second.get();
   }
-  JitEntry* e = it->second.get();
+  if (!e) {
+    auto ne = std::make_unique<JitEntry>();
+    ne->source = bfa::emit_kernel(p->parsed, spec, &ne->stats);
+    int rc = nvrtc_compile(ne->source, &ne->cubin);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->jit.find(key);
+    if (it == p->jit.end()) it = p->jit.emplace(key, std::move(ne)).first;
+    e = it->second.get();
+  }
   if (dev >= 0) {
+    std::lock_guard<std::mutex> lk(p->mu);
     auto f = e->fn.find(dev);
     if (f == e->fn.end()) {
       CUmodule mod;
@@ -313,6 +325,9 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     spec.thread_bits = o.thread_bits;
     spec.inner_bits = sg.generic ? 0 : sg.m;
     spec.fuse_count = eval && count_dev != nullptr;
+    spec.dual_pipe = o.dual_pipe;
+    spec.imad_cost_pct = o.imad_cost_pct;
+    spec.min_blocks = sg.generic ? 0 : o.min_blocks;
     JitEntry* je = nullptr;
     CUfunction fn;
     rc = get_kernel(p, spec, dev, &je, &fn);
@@ -342,7 +357,10 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
        << ", \"m\": " << spec.inner_bits << ", \"grid\": " << grid << ", \"block\": " << T
        << ", \"regs\": " << je->regs << ", \"blocks_per_sm\": " << bps
        << ", \"luts_thread\": " << je->stats.luts_thread << ", \"luts_outer\": " << je->stats.luts_outer
-       << ", \"luts_inner\": " << je->stats.luts_inner << ", \"words_per_iter\": " << je->stats.words_per_iter
+       << ", \"luts_inner\": " << je->stats.luts_inner << ", \"imads_thread\": " << je->stats.imads_thread
+       << ", \"imads_outer\": " << je->stats.imads_outer << ", \"imads_inner\": " << je->stats.imads_inner
+       << ", \"derived_outer\": " << je->stats.derived_outer << ", \"derived_inner\": " << je->stats.derived_inner
+       << ", \"imad_cost\": " << je->stats.imad_cost << ", \"words_per_iter\": " << je->stats.words_per_iter
        << ", \"inner_vars\": " << je->stats.inner_vars << ", \"outer_vars\": " << je->stats.outer_vars
        << ", \"thread_vars\": " << je->stats.thread_vars << "}";
   }
@@ -373,6 +391,9 @@ int spec_for_what(const bfa_prog* p, int what, bfa::KernelSpec* spec) {
   spec->slot_bits = spec->generic ? 0 : p->opt.slot_bits;
   spec->thread_bits = p->opt.thread_bits;
   spec->inner_bits = spec->generic ? 0 : p->opt.inner_bits;
+  spec->dual_pipe = p->opt.dual_pipe;
+  spec->imad_cost_pct = p->opt.imad_cost_pct;
+  spec->min_blocks = spec->generic ? 0 : p->opt.min_blocks;
   return BFA_OK;
 }
 
@@ -435,12 +456,15 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   std::lock_guard<std::mutex> lk(p->mu);
   std::string k(key);
   auto bad = [&]() { return set_err(BFA_E_ARG, "option %s=%lld out of range", key, (long long)v); };
-  if (k == "slot_bits") { if (v < 0 || v > 3) return bad(); p->opt.slot_bits = (int)v; }
+  if (k == "slot_bits") { if (v < 0 || v > 5) return bad(); p->opt.slot_bits = (int)v; }
   else if (k == "thread_bits") { if (v < 5 || v > 10) return bad(); p->opt.thread_bits = (int)v; }
   else if (k == "inner_bits") { if (v < 0 || v > 8) return bad(); p->opt.inner_bits = (int)v; }
   else if (k == "blocks_per_sm") { if (v < 0 || v > 32) return bad(); p->opt.blocks_per_sm = (int)v; }
   else if (k == "force_generic") { if (v < 0 || v > 1) return bad(); p->opt.force_generic = (int)v; }
   else if (k == "engine") { if (v < 0 || v > 1) return bad(); p->opt.engine = (int)v; }
+  else if (k == "dual_pipe") { if (v < 0 || v > 1) return bad(); p->opt.dual_pipe = (int)v; }
+  else if (k == "imad_cost_pct") { if (v < 0 || v > 1000) return bad(); p->opt.imad_cost_pct = (int)v; }
+  else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -476,6 +500,112 @@ int bfa_eval(const bfa_prog* p, int n, uint64_t* out) {
   return BFA_OK;
 }
 
+int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  if (p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "program uses x%d >= n", p->info.max_var_id);
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  std::ostringstream js;
+  if (n < 24 || p->opt.force_generic || p->opt.engine) {
+    js << "{\"skipped\": \"problem too small or generic/interpreter engine\"}";
+    if (report && len) snprintf(report, len, "%s", js.str().c_str());
+    return BFA_OK;
+  }
+  // probe: the top 2^k valuations (k <= 36), the same launch planning as a real call
+  const int k = std::min(n, 36);
+  const uint64_t hi = n == 63 ? (1ull << 63) : (1ull << n), lo = hi - (1ull << k);
+  const Options base = p->opt;
+  struct Cand { Options o; double ms = -1; int regs = 0; uint32_t cells = 0; };
+  std::vector<Cand> cands;
+  for (int sb : {2, 3, 4, 5})
+    for (int ic : {0, 35, 50}) {
+      Cand c; c.o = base;
+      c.o.slot_bits = sb; c.o.inner_bits = 4;
+      c.o.dual_pipe = ic ? 1 : 0; c.o.imad_cost_pct = ic;
+      cands.push_back(c);
+    }
+  for (int sb : {3, 4}) {
+    Cand c; c.o = base;
+    c.o.slot_bits = sb; c.o.inner_bits = 2; c.o.dual_pipe = 1; c.o.imad_cost_pct = 50;
+    cands.push_back(c);
+  }
+  // phase 1: compile every candidate's specialised kernel in parallel (host only)
+  const int T = 1 << base.thread_bits;
+  const int full_grid = di.sms * std::max(1, base.blocks_per_sm ? base.blocks_per_sm : 2048 / T / 2);
+  std::vector<bfa::KernelSpec> specs(cands.size());
+  std::vector<int> ok(cands.size(), 0);
+  for (size_t i = 0; i < cands.size(); i++) {
+    std::vector<Segment> segs = plan(cands[i].o, cands[i].o.slot_bits, n, lo >> 5, hi >> 5, full_grid);
+    for (const Segment& sg : segs)
+      if (!sg.generic) {
+        bfa::KernelSpec& sp = specs[i];
+        sp.mode = bfa::KM_COUNT; sp.generic = false; sp.slot_bits = cands[i].o.slot_bits;
+        sp.thread_bits = cands[i].o.thread_bits; sp.inner_bits = sg.m; sp.dual_pipe = cands[i].o.dual_pipe;
+        sp.imad_cost_pct = cands[i].o.imad_cost_pct; sp.min_blocks = cands[i].o.min_blocks;
+        ok[i] = 1;
+      }
+  }
+  {
+    std::vector<std::thread> th;
+    std::vector<int> rcs(cands.size(), 0);
+    for (size_t i = 0; i < cands.size(); i++)
+      if (ok[i]) th.emplace_back([&, i] { JitEntry* e = nullptr; rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
+                                          if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner; });
+    for (auto& t : th) t.join();
+    for (size_t i = 0; i < cands.size(); i++)
+      if (ok[i] && rcs[i]) ok[i] = 0;
+  }
+  // phase 2: time each candidate on the probe (module load + 1 untimed launch, best of 3)
+  uint64_t* d = nullptr;
+  if ((rc = scratch_u64(dev, &d))) return rc;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int best = -1;
+  for (size_t i = 0; i < cands.size(); i++) {
+    if (!ok[i] || cands[i].cells > 8192) continue;  // i-cache: skip very long bodies
+    p->opt = cands[i].o;
+    if ((rc = run_range(p, n, lo, hi, nullptr, d, st, false))) { p->opt = base; return rc; }
+    float bestms = 1e30f;
+    for (int r = 0; r < 3; r++) {
+      cudaEventRecord(e0, st);
+      run_range(p, n, lo, hi, nullptr, d, st, false);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      bestms = std::min(bestms, ms);
+    }
+    cands[i].ms = bestms;
+    JitEntry* e = nullptr;
+    get_kernel(p, specs[i], dev, &e, nullptr);
+    cands[i].regs = e ? e->regs : 0;
+    if (best < 0 || cands[i].ms < cands[best].ms) best = (int)i;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaError_t ce = cudaStreamSynchronize(st);
+  if (ce != cudaSuccess) { p->opt = base; return set_err(BFA_E_CUDA, "autotune: %s", cudaGetErrorString(ce)); }
+  p->opt = best >= 0 ? cands[best].o : base;
+  js << "{\"probe_valuations\": " << (hi - lo) << ", \"candidates\": [";
+  bool first = true;
+  for (size_t i = 0; i < cands.size(); i++) {
+    if (cands[i].ms < 0) continue;
+    js << (first ? "" : ", ") << "{\"slot_bits\": " << cands[i].o.slot_bits << ", \"inner_bits\": " << cands[i].o.inner_bits
+       << ", \"imad_cost_pct\": " << cands[i].o.imad_cost_pct << ", \"dual_pipe\": " << cands[i].o.dual_pipe
+       << ", \"ms\": " << cands[i].ms << ", \"regs\": " << cands[i].regs << ", \"cells\": " << cands[i].cells << "}";
+    first = false;
+  }
+  js << "], \"best\": {\"slot_bits\": " << p->opt.slot_bits << ", \"inner_bits\": " << p->opt.inner_bits
+     << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe << "}}";
+  if (report && len) snprintf(report, len, "%s", js.str().c_str());
+  return BFA_OK;
+}
+
 int bfa_fill_generators(int n, int n_rows, uint64_t* table_dev, void* stream) {
   if (!table_dev || n_rows < 0) return set_err(BFA_E_ARG, "bad argument");
   if (n < 7 || n > 40 || n_rows > n) return set_err(BFA_E_RANGE, "fill needs 7 <= n <= 40 and rows <= n");
@@ -497,14 +627,14 @@ int bfa_popcount(const uint64_t* vec_dev, uint64_t n_words, uint64_t* count_dev,
   return BFA_OK;
 }
 
-int bfa_peak_lop3(int blocks, int threads, int iters, uint32_t* sink_dev, void* stream) {
-  if (blocks <= 0 || threads <= 0 || threads > 1024 || iters <= 0 || !sink_dev)
+int bfa_peak_int(int op, int blocks, int threads, int iters, uint32_t* sink_dev, void* stream) {
+  if (op < 0 || op > 2 || blocks <= 0 || threads <= 0 || threads > 256 || iters <= 0 || !sink_dev)
     return set_err(BFA_E_ARG, "bad argument");
   int dev;
   int rc = current_device(&dev, nullptr);
   if (rc) return rc;
-  cudaError_t e = bfa_k::peak_lop3(blocks, threads, iters, sink_dev, (cudaStream_t)stream);
-  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "peak_lop3: %s", cudaGetErrorString(e));
+  cudaError_t e = bfa_k::peak_int(op, blocks, threads, iters, sink_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "peak_int: %s", cudaGetErrorString(e));
   return BFA_OK;
 }
 

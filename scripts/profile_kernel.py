@@ -1,7 +1,7 @@
 """Launch the bench's register-mode count kernel on a sub-range of a config
 (same JIT variant and launch geometry as bench.py), for ncu captures.
 
-    python scripts/profile_kernel.py [config] [log2_valuations] [launches]
+    python scripts/profile_kernel.py [config] [log2_valuations] [launches] [opt=v,opt=v]
 """
 import os
 import sys
@@ -17,6 +17,9 @@ k = int(sys.argv[2]) if len(sys.argv) > 2 else 36
 launches = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 text, n, _ = W.config(cfg)
 p = bfa.Program(text)
+for kv in filter(None, (sys.argv[4] if len(sys.argv) > 4 else "").split(",")):
+    a, b = kv.split("=")
+    p.set_option(a, int(b))
 cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 lo = (1 << n) - (1 << k)
 for _ in range(launches):

@@ -82,7 +82,8 @@ def test_random_terms(block):
 
 GEOMETRIES = [dict(slot_bits=0, thread_bits=5, inner_bits=0), dict(slot_bits=1, thread_bits=6, inner_bits=2),
               dict(slot_bits=3, thread_bits=7, inner_bits=3), dict(slot_bits=2, thread_bits=8, inner_bits=4),
-              dict(force_generic=1)]
+              dict(force_generic=1), dict(imad_cost_pct=20), dict(imad_cost_pct=20, force_generic=1),
+              dict(dual_pipe=0), dict(slot_bits=5, imad_cost_pct=50), dict(slot_bits=4, inner_bits=2, min_blocks=2)]
 
 
 @pytest.mark.parametrize("geo", range(len(GEOMETRIES)))
@@ -214,6 +215,19 @@ def test_c5_bench_config_subcubes():
         assert int(p.count_range(n, lo, hi).item()) == oracle.count(text, n, lo, hi)
         ow, _ = oracle.evaluate(text, n, lo, lo + (1 << 16))
         assert np.array_equal(host(p.eval_range(n, lo, lo + (1 << 16))), ow)
+
+
+def test_autotune_keeps_results():
+    """bfa_autotune only changes speed: C4 still counts 130023 and a
+    sub-cube vector still equals the oracle's after tuning."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text)
+    rep = p.autotune(n)
+    assert rep["best"] and len(rep["candidates"]) >= 6
+    assert p.count(n) == expect
+    lo = (1 << 36) - (1 << 22)
+    ow, oc = oracle.evaluate(text, n, lo, 1 << 36)
+    assert np.array_equal(host(p.eval_range(n, lo, 1 << 36)), ow)
 
 
 # ------------------------------------------------------------ materialised mode
