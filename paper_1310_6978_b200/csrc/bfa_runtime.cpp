@@ -533,12 +533,24 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
     c.o.slot_bits = sb; c.o.inner_bits = 2; c.o.dual_pipe = 1; c.o.imad_cost_pct = 50;
     cands.push_back(c);
   }
+  // occupancy for registers: cap at 128 (2 blocks of 256) or 168 (3 x 128)
+  for (int sb : {3, 4, 5}) {
+    Cand c; c.o = base;
+    c.o.slot_bits = sb; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35; c.o.min_blocks = 2;
+    cands.push_back(c);
+  }
+  {
+    Cand c; c.o = base;
+    c.o.slot_bits = 5; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35;
+    c.o.thread_bits = 7; c.o.min_blocks = 3;
+    cands.push_back(c);
+  }
   // phase 1: compile every candidate's specialised kernel in parallel (host only)
-  const int T = 1 << base.thread_bits;
-  const int full_grid = di.sms * std::max(1, base.blocks_per_sm ? base.blocks_per_sm : 2048 / T / 2);
   std::vector<bfa::KernelSpec> specs(cands.size());
   std::vector<int> ok(cands.size(), 0);
   for (size_t i = 0; i < cands.size(); i++) {
+    const int T = 1 << cands[i].o.thread_bits;
+    const int full_grid = di.sms * std::max(1, cands[i].o.blocks_per_sm ? cands[i].o.blocks_per_sm : 2048 / T / 2);
     std::vector<Segment> segs = plan(cands[i].o, cands[i].o.slot_bits, n, lo >> 5, hi >> 5, full_grid);
     for (const Segment& sg : segs)
       if (!sg.generic) {
@@ -597,11 +609,13 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
     if (cands[i].ms < 0) continue;
     js << (first ? "" : ", ") << "{\"slot_bits\": " << cands[i].o.slot_bits << ", \"inner_bits\": " << cands[i].o.inner_bits
        << ", \"imad_cost_pct\": " << cands[i].o.imad_cost_pct << ", \"dual_pipe\": " << cands[i].o.dual_pipe
+       << ", \"min_blocks\": " << cands[i].o.min_blocks << ", \"thread_bits\": " << cands[i].o.thread_bits
        << ", \"ms\": " << cands[i].ms << ", \"regs\": " << cands[i].regs << ", \"cells\": " << cands[i].cells << "}";
     first = false;
   }
   js << "], \"best\": {\"slot_bits\": " << p->opt.slot_bits << ", \"inner_bits\": " << p->opt.inner_bits
-     << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe << "}}";
+     << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
+     << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits << "}}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
   return BFA_OK;
 }
