@@ -53,7 +53,13 @@ def parse_args():
     return ap.parse_args()
 
 
+MATERIALISED = {"c2": ("c2", 0), "c2_fused": ("c2", 1), "c2_n32": ("c2_n32", 0), "c2_n32_fused": ("c2_n32", 1)}
+
 CONFIG_DESC = {
+    "c2": "random 3-CNF, 2000 clauses over n=28, materialised vector algebra (HBM) + popcount (BASELINE configs[1])",
+    "c2_fused": "random 3-CNF, 2000 clauses over n=28, materialised table S, fused 128-bit-load kernel + popcount",
+    "c2_n32": "random 3-CNF, 2000 clauses over n=32 (512 MiB vectors >> L2), materialised vector algebra + popcount",
+    "c2_n32_fused": "random 3-CNF, 2000 clauses over n=32, materialised table S, fused kernel + popcount",
     "c5": "random 1000-gate Boolean DAG over n=42 vars, count mode (BASELINE configs[4])",
     "c4": "labeled partial orders on 6 points, n=36, count mode (BASELINE configs[3])",
     "c3_posets": "labeled partial orders on 5 points, n=25, count mode (BASELINE configs[2])",
@@ -349,10 +355,94 @@ def run_bfa(args):
         dist.destroy_process_group()
 
 
+def hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else
+    the profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs (measured copy)"
+    except (OSError, KeyError, ValueError):
+        return 6650e9, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def run_materialised(args):
+    """The paper's vector formulation: generator table S in
+    HBM, full-vector LOP3 passes (variant 0) or fused 128-bit loads (variant
+    1), popcount.  One GPU; a step = one full evaluation + count."""
+    import torch
+
+    import paper_1310_6978_b200 as bfa
+    if int(os.environ.get("WORLD_SIZE", "1")) != 1:
+        raise SystemExit("materialised configs run on one GPU")
+    torch.cuda.set_device(0)
+    cfg, variant = MATERIALISED[args.config]
+    text, n, expect = W.config(cfg)
+    prog = bfa.Program(text)
+    info = prog.info
+    out = torch.empty(bfa.words_for(n), dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
+    torch.cuda.synchronize()
+    launch = bfa.last_launch()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    clocks = ClockSampler(0)
+    clocks.start()
+    time.sleep(0.2)
+    ms = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
+        e.record(stream)
+        torch.cuda.synchronize()
+        ms.append(s.elapsed_time(e))
+    clk = clocks.stop()
+    t = sum(ms) / 1e3 / args.steps
+    vbytes = (1 << n) // 8
+    fill = n * vbytes
+    popc = vbytes
+    if variant == 0:
+        logical = launch.get("logical_bytes", 0) + fill + popc
+    else:
+        logical = fill + (launch.get("rows_loaded", n) + 1) * vbytes + popc
+    peak, src = hbm_peak()
+    # e2e: host buffers -- the vector copied back to pinned host memory each step
+    host = torch.empty(out.numel(), dtype=torch.int64, pin_memory=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
+        host.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e = (1 << n) * args.steps / (time.perf_counter() - t0)
+    line = {"metric": "valuations/s", "value": (1 << n) / t, "unit": "valuations/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 (bitwise, 128-bit vector accesses)",
+            "data": "synthetic (seeded generator, workloads/__init__.py)",
+            "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "n": n, "clauses": 2000,
+                       "luts_L": info["luts"], "gates_G": info["gates"], "seed": W.SEED,
+                       "l2": "L2 flushed (256 MiB write) before every timed step; n=28 vectors (32 MiB) can be "
+                             "L2-resident within a step, n=32 (512 MiB) cannot"},
+            "count": int(cnt.item()), "count_expected": expect,
+            "roofline": {"bound": "hbm", "achieved": logical / t / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                         "frac": logical / t / peak, "traffic": None, "peak_source": src,
+                         "per_unit": "logical bytes = table fill n*2^n/8 + sum over passes (arity+1)*2^n/8 "
+                                     "(variant 0) or (|supp|+1)*2^n/8 (variant 1) + popcount 2^n/8",
+                         "logical_bytes_per_step": logical},
+            "e2e": {"value": e2e, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": vbytes,
+                    "call": "bfa_eval_materialised + vector D2H to pinned host"},
+            "gpu_launches": launch.get("kernels", 0) * args.steps, "launch": launch, "clocks": clk}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.config in MATERIALISED:
+        run_materialised(args)
     else:
         run_bfa(args)
 

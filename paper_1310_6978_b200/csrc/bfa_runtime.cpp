@@ -675,6 +675,20 @@ int bfa_eval_materialised(const bfa_prog* p, int n, int variant, uint64_t* out_d
     allocs.push_back(*ptr);
     return BFA_OK;
   };
+  {
+    // keep freed scratch mapped in the device's stream-ordered pool between calls
+    static std::mutex pmu;
+    static std::map<int, bool> tuned;
+    std::lock_guard<std::mutex> lk(pmu);
+    if (!tuned[dev]) {
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      }
+      tuned[dev] = true;
+    }
+  }
   const int rows = n;  // the paper's table S: n rows of 2^n bits
   uint64_t* table = nullptr;
   if ((rc = alloc((void**)&table, vbytes * rows))) { cleanup(); return rc; }
@@ -739,6 +753,29 @@ int bfa_eval_materialised(const bfa_prog* p, int n, int variant, uint64_t* out_d
       kernels++;
       logical_bytes += 2 * vbytes;
     } else {
+      // Depth-first (post-order) pass schedule from the root: a finished
+      // subtree leaves one live vector, so the live set stays near the tree
+      // depth (node-id order would keep e.g. every CNF clause vector alive).
+      {
+        std::map<uint32_t, size_t> at;
+        for (size_t k = 0; k < mr.luts.size(); k++) at[mr.luts[k].root] = k;
+        std::vector<bfa::Lut> order;
+        std::vector<uint8_t> done(mr.luts.size(), 0);
+        std::vector<std::pair<size_t, int>> st{{at.at(bfa::lit_node(root)), 0}};
+        while (!st.empty()) {
+          auto& [k, q] = st.back();
+          if (done[k]) { st.pop_back(); continue; }
+          if (q < mr.luts[k].nin) {
+            auto it = at.find(mr.luts[k].in[q++]);
+            if (it != at.end() && !done[it->second]) st.push_back({it->second, 0});
+            continue;
+          }
+          done[k] = 1;
+          order.push_back(mr.luts[k]);
+          st.pop_back();
+        }
+        mr.luts.swap(order);
+      }
       // last use of every LUT result
       std::map<uint32_t, size_t> pos, last;
       for (size_t k = 0; k < mr.luts.size(); k++) pos[mr.luts[k].root] = k;

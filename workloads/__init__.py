@@ -280,6 +280,8 @@ def config(name: str):
         return cnf3(28, 2000), 28, 0
     if name == "c2_m100":
         return cnf3(28, 100), 28, None
+    if name == "c2_n32":
+        return cnf3(32, 2000), 32, 0
     if name == "c3_equiv":
         return equivalences(5), 25, 52
     if name == "c3_posets":
