@@ -896,6 +896,83 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   return os.str();
 }
 
+InterpProgram build_interp(const Parsed& prog) {
+  // the generic specialisation: lanes 0-4 as word constants, variables >= 5
+  // computed from the word index; plain LUT3 cover
+  Dag D;
+  std::vector<Lit> subst(64);
+  for (int v = 0; v < 64; v++) subst[v] = v < 5 ? D.word(kLane[v]) : D.var((uint32_t)v);
+  std::vector<uint8_t> done(prog.dag.nodes.size());
+  std::vector<Lit> memo(prog.dag.nodes.size());
+  Lit out = rebuild(prog.dag, prog.root, subst, D, memo, done);
+  std::vector<uint8_t> lv(64, 3);
+  const double w[4] = {0, 1, 1, 1};
+  MapResult mr = map_luts(D, {out}, lv, w);
+  InterpProgram ip;
+  // value list in evaluation order: used variables first, then LUT roots
+  std::vector<uint32_t> order;
+  std::vector<uint8_t> isvar(D.nodes.size(), 0);
+  for (const Lut& L : mr.luts)
+    for (int q = 0; q < 3; q++)
+      if (D.nodes[L.in[q]].kind == NK_VAR && !isvar[L.in[q]]) { isvar[L.in[q]] = 1; order.push_back(L.in[q]); }
+  if (D.nodes[lit_node(out)].kind == NK_VAR && !isvar[lit_node(out)]) { isvar[lit_node(out)] = 1; order.push_back(lit_node(out)); }
+  std::map<uint32_t, const Lut*> lut_of;
+  for (const Lut& L : mr.luts) { order.push_back(L.root); lut_of[L.root] = &L; }
+  // last use (index in `order`) of every value; the output lives to the end
+  std::map<uint32_t, size_t> last;
+  for (size_t k = 0; k < order.size(); k++) {
+    auto it = lut_of.find(order[k]);
+    if (it != lut_of.end())
+      for (int q = 0; q < 3; q++) last[it->second->in[q]] = k;
+  }
+  last[lit_node(out)] = order.size();
+  std::map<uint32_t, uint32_t> constidx;
+  auto cst = [&](uint32_t word) -> uint32_t {
+    auto it = constidx.find(word);
+    if (it != constidx.end()) return it->second;
+    uint32_t i = (uint32_t)ip.consts.size();
+    ip.consts.push_back(word);
+    constidx[word] = i;
+    return i;
+  };
+  std::map<uint32_t, uint32_t> slot;
+  std::vector<uint32_t> free_slots;
+  auto operand = [&](uint32_t n) -> uint32_t {
+    if (D.nodes[n].kind == NK_CONST) return 0x80000000u | cst(D.nodes[n].val);
+    return slot.at(n);
+  };
+  for (size_t k = 0; k < order.size(); k++) {
+    const uint32_t n = order[k];
+    uint32_t a = 0, b = 0, c = 0, imm = 0, kind = 1;
+    auto it = lut_of.find(n);
+    if (it != lut_of.end()) {
+      const Lut& L = *it->second;
+      kind = 0; imm = L.imm;
+      a = operand(L.in[0]); b = operand(L.in[1]); c = operand(L.in[2]);
+      // inputs whose last use is this op free their slots before dst is chosen
+      for (int q = 0; q < 3; q++) {
+        uint32_t in = L.in[q];
+        if (D.nodes[in].kind != NK_CONST && last[in] == k && slot.count(in)) {
+          bool dup = false;
+          for (int r = 0; r < q; r++) dup |= L.in[r] == in;
+          if (!dup) free_slots.push_back(slot[in]);
+        }
+      }
+    } else {
+      a = D.nodes[n].val - 5;
+    }
+    uint32_t dst;
+    if (!free_slots.empty()) { dst = free_slots.back(); free_slots.pop_back(); }
+    else dst = ip.n_slots++;
+    slot[n] = dst;
+    ip.ops.insert(ip.ops.end(), {dst | (imm << 16) | (kind << 24), a, b, c});
+  }
+  const Node& on = D.nodes[lit_node(out)];
+  if (on.kind == NK_CONST) ip.out = 0x80000000u | cst(lit_neg(out) ? ~on.val : on.val);
+  else { ip.out = slot.at(lit_node(out)); ip.out_neg = lit_neg(out); }
+  return ip;
+}
+
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts) {
   Dag D;
   std::vector<Lit> subst(64);

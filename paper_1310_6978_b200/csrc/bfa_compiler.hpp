@@ -134,6 +134,20 @@ struct KernelStats {
 // CUDA C++ source of one kernel variant (entry point "bfa_kernel").
 std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);
 
+// Program for the constant-memory interpreter (engine=1, the ablation of the
+// JIT): ops are uint4 {dst | imm << 16 | kind << 24, a, b, c}; kind 0 = LOP3
+// over operands a, b, c, kind 1 = generator word of variable (a + 5) from the
+// word index.  An operand with bit 31 set is consts[operand & 0xff], else a
+// value slot.  Slots are reused by liveness.
+struct InterpProgram {
+  std::vector<uint32_t> ops;     // 4 words per op
+  std::vector<uint32_t> consts;
+  uint32_t n_slots = 0;
+  uint32_t out = 0;              // operand encoding of the result
+  bool out_neg = false;
+};
+InterpProgram build_interp(const Parsed& prog);
+
 // LUT cover IR text (bfa_dump what=0) and the plain cover size L.
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts);
 

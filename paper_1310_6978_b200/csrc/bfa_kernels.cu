@@ -10,6 +10,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <mutex>
+
 #include "bfa_kernels.hpp"
 
 namespace {
@@ -163,6 +166,64 @@ __global__ void __launch_bounds__(256) peak_mix_kernel(u32* sink, int iters, u32
   if (acc == 0x12345678u) sink[blockIdx.x] = acc;
 }
 
+// ---------------------------------------------------------------- interpreter
+// The ablation of the JIT (engine=1): the LUT program is read from constant
+// memory and interpreted per 32-bit word; values live in shared memory,
+// one column per thread (slot * blockDim + tid: conflict-free).  Each op is a
+// warp-uniform switch on its 8-bit LUT to a lop3 with that immediate.
+__constant__ uint4 c_interp_ops[3800];
+__constant__ u32 c_interp_consts[256];
+
+template <int IMM>
+__device__ __forceinline__ u32 lop(u32 a, u32 b, u32 c) {
+  u32 d;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(d) : "r"(a), "r"(b), "r"(c), "n"(IMM));
+  return d;
+}
+
+__device__ __forceinline__ u32 lop3_dyn(u32 imm, u32 a, u32 b, u32 c) {
+  switch (imm) {
+#define BFA_C1(i) case (i): return lop<(i)>(a, b, c);
+#define BFA_C4(i) BFA_C1(i) BFA_C1(i + 1) BFA_C1(i + 2) BFA_C1(i + 3)
+#define BFA_C16(i) BFA_C4(i) BFA_C4(i + 4) BFA_C4(i + 8) BFA_C4(i + 12)
+#define BFA_C64(i) BFA_C16(i) BFA_C16(i + 16) BFA_C16(i + 32) BFA_C16(i + 48)
+    BFA_C64(0) BFA_C64(64) BFA_C64(128) BFA_C64(192)
+#undef BFA_C64
+#undef BFA_C16
+#undef BFA_C4
+#undef BFA_C1
+  }
+  return 0;
+}
+
+__device__ __forceinline__ u32 interp_fetch(const u32* vals, u32 x, u32 T, u32 tid) {
+  return (x & 0x80000000u) ? c_interp_consts[x & 0xffu] : vals[x * T + tid];
+}
+
+__global__ void __launch_bounds__(256) interp_kernel(int n_ops, u32 out_op, u32 out_neg, u64 w_begin, u64 w_count,
+                                                     u32 mask, u32* __restrict__ out, u64* count) {
+  extern __shared__ u32 vals[];
+  const u32 T = blockDim.x, tid = threadIdx.x;
+  u64 acc = 0;
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 k = (u64)blockIdx.x * blockDim.x + tid; k < w_count; k += stride) {
+    const u64 w = w_begin + k;
+    for (int i = 0; i < n_ops; i++) {
+      const uint4 op = c_interp_ops[i];
+      const u32 dst = op.x & 0xffffu;
+      u32 v;
+      if ((op.x >> 24) == 1u) v = 0u - (u32)((w >> op.y) & 1ull);
+      else v = lop3_dyn((op.x >> 16) & 0xffu, interp_fetch(vals, op.y, T, tid), interp_fetch(vals, op.z, T, tid),
+                        interp_fetch(vals, op.w, T, tid));
+      vals[dst * T + tid] = v;
+    }
+    const u32 r = (interp_fetch(vals, out_op, T, tid) ^ (out_neg ? ~0u : 0u)) & mask;
+    if (out) out[k] = r;
+    acc += __popc(r);
+  }
+  if (count) block_sum_add(acc, count);
+}
+
 int grid_for(u64 items, int threads) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -202,6 +263,36 @@ cudaError_t popcount(const uint64_t* v, uint64_t n_words, uint64_t* count, cudaS
       reinterpret_cast<const uint4*>(v), pairs, reinterpret_cast<const u64*>(v) + (n_words - 1), has_tail,
       reinterpret_cast<u64*>(count));
   return cudaGetLastError();
+}
+
+cudaError_t interp(const uint32_t* ops, int n_ops, const uint32_t* consts, int n_consts, int n_slots,
+                   uint32_t out_op, int out_neg, uint64_t w_begin, uint64_t w_count, uint32_t mask, uint32_t* out,
+                   uint64_t* count, cudaStream_t st, int* block_used) {
+  if (n_ops > 3800 || n_consts > 256) return cudaErrorInvalidValue;
+  static std::mutex mu;  // the program symbol is process-global: one launch at a time
+  std::lock_guard<std::mutex> lk(mu);
+  int T = 256;
+  const size_t per = (size_t)std::max(1, n_slots) * 4;
+  while (T > 32 && per * T > 200 * 1024) T -= 32;
+  if (per * T > 200 * 1024) return cudaErrorInvalidValue;
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_interp_ops, ops, (size_t)n_ops * 16, 0, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && n_consts)
+    e = cudaMemcpyToSymbolAsync(c_interp_consts, consts, (size_t)n_consts * 4, 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const size_t smem = per * T;
+  cudaFuncSetAttribute(interp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148, nb = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, interp_kernel, T, smem);
+  u64 need = (w_count + T - 1) / T;
+  u64 grid = std::min<u64>(std::max<u64>(need, 1), (u64)sms * std::max(1, nb));
+  interp_kernel<<<(unsigned)grid, T, smem, st>>>(n_ops, out_op, (u32)out_neg, w_begin, w_count, mask, out,
+                                                  reinterpret_cast<u64*>(count));
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the symbol may be rewritten after we return
+  if (block_used) *block_used = T;
+  return e;
 }
 
 cudaError_t peak_int(int op, int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st) {

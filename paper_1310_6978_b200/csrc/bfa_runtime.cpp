@@ -170,6 +170,7 @@ struct bfa_prog {
   Options opt;
   std::mutex mu;
   std::map<std::string, std::unique_ptr<JitEntry>> jit;
+  std::unique_ptr<bfa::InterpProgram> interp;  // engine=1 ablation
 };
 
 namespace {
@@ -267,7 +268,6 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   if (p->info.max_var_id >= n)
     return set_err(BFA_E_RANGE, "program uses x%d, needs n > %d (got n=%d)", p->info.max_var_id,
                    p->info.max_var_id, n);
-  if (p->opt.engine != 0) return set_err(BFA_E_ARG, "engine=%d not available in this build", p->opt.engine);
   const uint64_t full = 1ull << n;
   if (mu_lo > mu_hi || mu_hi > full) return set_err(BFA_E_RANGE, "valuation range outside [0, 2^n)");
   const bool whole = mu_lo == 0 && mu_hi == full;
@@ -302,6 +302,26 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   if (whi == wlo) return BFA_OK;
 
   const Options& o = p->opt;
+  if (o.engine == 1) {
+    // constant-memory interpreter (ablation of the JIT)
+    bfa_prog* mp = const_cast<bfa_prog*>(p);
+    {
+      std::lock_guard<std::mutex> lk(mp->mu);
+      if (!mp->interp) mp->interp = std::make_unique<bfa::InterpProgram>(bfa::build_interp(p->parsed));
+    }
+    const bfa::InterpProgram& ip = *p->interp;
+    int T = 0;
+    cudaError_t e = bfa_k::interp(ip.ops.data(), (int)(ip.ops.size() / 4), ip.consts.data(), (int)ip.consts.size(),
+                                  (int)ip.n_slots, ip.out, ip.out_neg ? 1 : 0, wlo, whi - wlo, mask,
+                                  eval ? reinterpret_cast<uint32_t*>(out_dev) : nullptr, count_dev, st, &T);
+    if (e != cudaSuccess) return set_err(BFA_E_CUDA, "interpreter: %s (ops %zu, slots %u)", cudaGetErrorString(e),
+                                         ip.ops.size() / 4, ip.n_slots);
+    std::ostringstream js;
+    js << "{\"device\": " << dev << ", \"engine\": \"interpreter\", \"ops\": " << ip.ops.size() / 4
+       << ", \"slots\": " << ip.n_slots << ", \"block\": " << T << ", \"kernels\": 1}";
+    g_last_launch = js.str();
+    return BFA_OK;
+  }
   const int T = 1 << o.thread_bits;
   // full-chip grid estimate for planning (exact occupancy comes from the kernel)
   const int full_grid = di.sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);

@@ -36,7 +36,9 @@ for spec in sys.argv[3:]:
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / reps
-    L = bfa.last_launch()["segments"]
+    ll = bfa.last_launch()
+    L = ll.get("segments") or [{"words": 0, "regs": None, "blocks_per_sm": None, "luts_inner": ll.get("ops"),
+                                "imads_inner": 0, "derived_inner": 0, "imad_cost": None}]
     g = max(L, key=lambda x: x["words"])
     print(json.dumps({"cfg": cfg, "opts": spec, "ms": round(ms, 3), "Gval_per_s": round((hi - lo) / ms / 1e6, 1),
                       "ok": c == ref, "count": c, "jit_s": round(jit, 2), "regs": g["regs"], "bps": g["blocks_per_sm"],

@@ -83,7 +83,8 @@ def test_random_terms(block):
 GEOMETRIES = [dict(slot_bits=0, thread_bits=5, inner_bits=0), dict(slot_bits=1, thread_bits=6, inner_bits=2),
               dict(slot_bits=3, thread_bits=7, inner_bits=3), dict(slot_bits=2, thread_bits=8, inner_bits=4),
               dict(force_generic=1), dict(imad_cost_pct=20), dict(imad_cost_pct=20, force_generic=1),
-              dict(dual_pipe=0), dict(slot_bits=5, imad_cost_pct=50), dict(slot_bits=4, inner_bits=2, min_blocks=2)]
+              dict(dual_pipe=0), dict(slot_bits=5, imad_cost_pct=50), dict(slot_bits=4, inner_bits=2, min_blocks=2),
+              dict(engine=1)]
 
 
 @pytest.mark.parametrize("geo", range(len(GEOMETRIES)))
