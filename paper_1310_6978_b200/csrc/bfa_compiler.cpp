@@ -680,84 +680,171 @@ const char* kPrelude =
 
 }  // namespace
 
-std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats) {
-  KernelStats st;
-  std::ostringstream os;
-  os << "// generated by libbfa: " << (spec.mode == KM_COUNT ? "count" : "eval")
-     << (spec.generic ? " generic" : " specialised") << " s=" << spec.slot_bits << " t=" << spec.thread_bits
-     << " m=" << spec.inner_bits << "\n" << kPrelude;
+// The specialised DAG of one kernel variant: the 2^s slot cofactors of f
+// with lane words as constants, and the loop level of every variable from
+// its bit position in the word index (spec.perm maps variable -> position;
+// empty = identity).
+struct Built {
+  Dag D;
+  std::vector<Lit> outs;
+  std::vector<uint8_t> var_level;
+  std::vector<int> pos;
+  double w[4];
+  int S = 1, s = 0, t = 8, m = 0;
+};
 
-  const int S = spec.generic ? 1 : (1 << spec.slot_bits);
-  const int s = spec.generic ? 0 : spec.slot_bits;
-  const int t = spec.thread_bits, m = spec.inner_bits;
-  const bool want_count = spec.mode == KM_COUNT || spec.fuse_count;
-
-  // roles of word-index bit p = v - 5:
+static void build_specialised(const Parsed& prog, const KernelSpec& spec, Built* b) {
+  b->S = spec.generic ? 1 : (1 << spec.slot_bits);
+  b->s = spec.generic ? 0 : spec.slot_bits;
+  b->t = spec.thread_bits;
+  b->m = spec.inner_bits;
+  const int s = b->s, t = b->t, m = b->m;
+  b->pos.resize(64);
+  for (int v = 0; v < 64; v++) b->pos[v] = (v < (int)spec.perm.size()) ? spec.perm[v] : v;
+  // roles of word-index bit p = pos(v) - 5:
   //   generic:     every v >= 5 is level 3, read from w
   //   specialised: p < s slot (constant per slot), < s+t thread (1),
   //                < s+t+m inner (3), else outer (2)
   auto level_of = [&](int v) -> int {
     if (spec.materialised) return 3;
-    if (v < 5) return 0;
-    int p = v - 5;
+    const int q = b->pos[v];
+    if (q < 5) return 0;
+    int p = q - 5;
     if (spec.generic) return 3;
     if (p < s) return 0;
     if (p < s + t) return 1;
     if (p < s + t + m) return 3;
     return 2;
   };
-  Dag D;
-  std::vector<Lit> outs;
   std::vector<uint8_t> done(prog.dag.nodes.size());
   std::vector<Lit> memo(prog.dag.nodes.size());
-  for (int slot = 0; slot < S; slot++) {
+  for (int slot = 0; slot < b->S; slot++) {
     std::vector<Lit> subst(64, 0);
     for (int v = 0; v < 64; v++) {
-      if (v < 5 && !spec.materialised) subst[v] = D.word(kLane[v]);
-      else if (!spec.generic && v - 5 < s) subst[v] = ((slot >> (v - 5)) & 1) ? D.const1() : D.const0();
-      else subst[v] = D.var((uint32_t)v);
+      const int q = b->pos[v];
+      if (q < 5 && !spec.materialised) subst[v] = b->D.word(kLane[q]);
+      else if (!spec.generic && !spec.materialised && q - 5 < s)
+        subst[v] = ((slot >> (q - 5)) & 1) ? b->D.const1() : b->D.const0();
+      else subst[v] = b->D.var((uint32_t)v);
     }
     std::fill(done.begin(), done.end(), 0);
-    outs.push_back(rebuild(prog.dag, prog.root, subst, D, memo, done));
+    b->outs.push_back(rebuild(prog.dag, prog.root, subst, b->D, memo, done));
   }
-  std::vector<uint8_t> var_level(64, 0);
-  for (int v = 0; v < 64; v++) var_level[v] = (uint8_t)level_of(v);
+  b->var_level.assign(64, 0);
+  for (int v = 0; v < 64; v++) b->var_level[v] = (uint8_t)level_of(v);
   const double iters_inner = (double)(1u << m);
-  const double w[4] = {0.0, 1e-4, spec.generic ? 1.0 : 1.0 / iters_inner, 1.0};
+  b->w[0] = 0.0;
+  b->w[1] = 1e-4;
+  b->w[2] = spec.generic ? 1.0 : 1.0 / iters_inner;
+  b->w[3] = 1.0;
+}
 
-  // Technology mapping.  With dual_pipe, gates that have a word-uniform input
-  // may become IMAD cells (FMA pipe) instead of being absorbed into LOP3 cells
-  // (ALU pipe); sweep the IMAD:LOP3 cost ratio and keep the cover minimising
-  // the modelled time per thread-iteration, max(2 A, 2 F, A + F + other):
-  // the ALU pipe takes a LOP3 and the FMA pipe an IMAD warp-instruction every
-  // 2 cycles per SMSP, and the scheduler issues one per cycle (bfa_peak_int
-  // measures 18.5 T LOP3/s, 18.5 T IMAD/s and 35.2 T/s for a 1:1 mix).
-  auto model = [&](const MapResult& r, double* A_out, double* F_out) {
-    double A = 0, F = 0;
-    Emitter probe(D, os);
-    for (const Lut& L : r.luts) {
-      if (L.kind == 1) { F += w[L.level]; probe.plan_cell(L); }
-      else A += w[L.level];
-    }
-    std::vector<uint8_t> lvl = r.node_level;
-    for (auto& kv : probe.derived) F += w[lvl[kv.first]] * (double)kv.second.size();
-    const double other = spec.generic ? 4.0 : S + S / 2.0 + 2.0 + 2.0 * m;
-    if (A_out) *A_out = A;
-    if (F_out) *F_out = F;
-    return std::max({2 * (A + other), 2 * F, A + F + other});
-  };
-  MapResult mr = map_luts(D, outs, var_level, w, 0.0);
-  double best = model(mr, nullptr, nullptr);
-  st.imad_cost = 0.0;
-  if (spec.dual_pipe && !spec.materialised) {
-    std::vector<double> sweep = {0.6, 0.75, 0.9, 1.0, 1.15, 1.3, 1.6, 2.0, 3.0};
-    if (spec.imad_cost_pct > 0) { sweep = {spec.imad_cost_pct / 100.0}; best = 1e300; }
-    for (double c : sweep) {
-      MapResult r = map_luts(D, outs, var_level, w, c);
-      double tm = model(r, nullptr, nullptr);
-      if (tm < best - 1e-9) { best = tm; mr = std::move(r); st.imad_cost = c; }
-    }
+// Modelled time per thread-iteration of a cover, max(2 A, 2 F, A + F + other):
+// the ALU pipe takes a LOP3 and the FMA pipe an IMAD warp-instruction every 2
+// cycles per SMSP, and the scheduler issues one per cycle (bfa_peak_int
+// measures 18.5 T LOP3/s, 18.5 T IMAD/s and 35.2 T/s for a 1:1 mix).
+static double model_time(const Built& b, const MapResult& r, const KernelSpec& spec) {
+  double A = 0, F = 0;
+  std::ostringstream sink;
+  Emitter probe(b.D, sink);
+  for (const Lut& L : r.luts) {
+    if (L.kind == 1) { F += b.w[L.level]; probe.plan_cell(L); }
+    else A += b.w[L.level];
   }
+  for (auto& kv : probe.derived) F += b.w[r.node_level[kv.first]] * (double)kv.second.size();
+  const double other = spec.generic ? 4.0 : b.S + b.S / 2.0 + 2.0 + 2.0 * b.m;
+  return std::max({2 * (A + other), 2 * F, A + F + other});
+}
+
+// Technology mapping.  With dual_pipe, gates that have a word-uniform input
+// may become IMAD cells (FMA pipe) instead of being absorbed into LOP3 cells
+// (ALU pipe); sweep the IMAD:LOP3 cost ratio (or use the fixed one) and keep
+// the cover with the least modelled time.
+static MapResult choose_mapping(const Built& b, const KernelSpec& spec, double* best_time, double* chosen) {
+  MapResult mr;
+  double best = 1e300, cost = 0.0;
+  std::vector<double> sweep = {0.0};
+  if (spec.dual_pipe && !spec.materialised) {
+    if (spec.imad_cost_pct > 0) sweep = {spec.imad_cost_pct / 100.0};
+    else sweep = {0.0, 0.6, 0.75, 0.9, 1.0, 1.15, 1.3, 1.6, 2.0, 3.0};
+  }
+  for (double c : sweep) {
+    MapResult r = map_luts(b.D, b.outs, b.var_level, b.w, c);
+    double tm = model_time(b, r, spec);
+    if (tm < best - 1e-9) { best = tm; mr = std::move(r); cost = c; }
+  }
+  if (best_time) *best_time = best;
+  if (chosen) *chosen = cost;
+  return mr;
+}
+
+double model_cost(const Parsed& prog, const KernelSpec& spec) {
+  Built b;
+  build_specialised(prog, spec, &b);
+  double t = 0;
+  choose_mapping(b, spec, &t, nullptr);
+  return t;
+}
+
+std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int k_free, int budget, uint64_t seed) {
+  // Count mode over an aligned sub-cube of 2^k_free valuations: any
+  // permutation of the variables below k_free is a bijection of the sub-cube,
+  // so the count is unchanged; search the one whose cover is cheapest.
+  k_free = std::min(k_free, 63);
+  KernelSpec spec = base;
+  std::vector<int8_t> perm(64);
+  for (int v = 0; v < 64; v++) perm[v] = (int8_t)v;
+  if (k_free <= 5 || spec.generic || spec.materialised || spec.mode != KM_COUNT) return {};
+  const int s = spec.slot_bits, t = spec.thread_bits, m = spec.inner_bits;
+  auto role = [&](int q) { return q < 5 ? 0 : q - 5 < s ? 1 : q - 5 < s + t ? 2 : q - 5 < s + t + m ? 3 : 4; };
+  auto eval = [&](const std::vector<int8_t>& pm) {
+    spec.perm = pm;
+    return model_cost(prog, spec);
+  };
+  uint64_t rs = seed * 6364136223846793005ull + 1442695040888963407ull;
+  auto rnd = [&](uint64_t n) { rs = rs * 6364136223846793005ull + 1442695040888963407ull; return (rs >> 33) % n; };
+  std::vector<int8_t> best = perm;
+  double best_c = eval(best);
+  int evals = 1;
+  // random restarts: shuffle the free variables' positions
+  for (int r = 0; r < std::max(1, budget / 4) && evals < budget; r++) {
+    std::vector<int8_t> pm = perm;
+    for (int i = k_free - 1; i > 0; i--) std::swap(pm[i], pm[rnd((uint64_t)i + 1)]);
+    double c = eval(pm);
+    evals++;
+    if (c < best_c) { best_c = c; best = pm; }
+  }
+  // hill climbing: swap the positions of two variables with different roles
+  while (evals < budget) {
+    int a = (int)rnd((uint64_t)k_free), c = (int)rnd((uint64_t)k_free);
+    if (role(best[a]) == role(best[c])) continue;
+    std::vector<int8_t> pm = best;
+    std::swap(pm[a], pm[c]);
+    double cc = eval(pm);
+    evals++;
+    if (cc < best_c) { best_c = cc; best = pm; }
+  }
+  bool identity = true;
+  for (int v = 0; v < 64; v++) identity &= best[v] == v;
+  return identity ? std::vector<int8_t>{} : best;
+}
+
+std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats) {
+  KernelStats st;
+  std::ostringstream os;
+  os << "// generated by libbfa: " << (spec.mode == KM_COUNT ? "count" : "eval")
+     << (spec.generic ? " generic" : " specialised") << " s=" << spec.slot_bits << " t=" << spec.thread_bits
+     << " m=" << spec.inner_bits << (spec.perm.empty() ? "" : " (permuted roles)") << "\n" << kPrelude;
+  Built b;
+  build_specialised(prog, spec, &b);
+  Dag& D = b.D;
+  const std::vector<Lit>& outs = b.outs;
+  const int S = b.S, s = b.s, t = b.t, m = b.m;
+  const bool want_count = spec.mode == KM_COUNT || spec.fuse_count;
+  auto level_of = [&](int v) { return (int)b.var_level[v]; };
+  auto pos = [&](int v) { return b.pos[v]; };
+  double best_t = 0;
+  MapResult mr = choose_mapping(b, spec, &best_t, &st.imad_cost);
 
   // which variables are referenced (as cell inputs or outputs)
   std::vector<uint8_t> used(64, 0);
@@ -826,8 +913,8 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
        << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
        << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += stride) {\n"
        << "    const u64 w = w_begin + k;\n";
-    for (int v = 5; v < 64; v++)
-      if (used[v]) declare_var(v, "0u - (u32)((w >> " + std::to_string(v - 5) + ") & 1ull)", "    ");
+    for (int v = 0; v < 64; v++)
+      if (used[v]) declare_var(v, "0u - (u32)((w >> " + std::to_string(pos(v) - 5) + ") & 1ull)", "    ");
     emit_level(3, "    ");
     os << "    const u32 r = (" << E.value(outs[0]) << ") & mask;\n";
     if (spec.mode == KM_EVAL) os << "    out[k] = r;\n";
@@ -836,7 +923,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     if (want_count) os << "  bfa_block_sum(acc, count);\n";
     os << "}\n";
     st.words_per_iter = 1;
-    for (int v = 5; v < 64; v++) st.inner_vars += used[v];
+    for (int v = 0; v < 64; v++) st.inner_vars += used[v];
   } else {
     const int unit = s + t + m;
     os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
@@ -845,27 +932,27 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
        << "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n"
        << "  const u64 o_begin = b * q + (b < rr ? b : rr);\n"
        << "  const u64 o_end = o_begin + q + (b < rr ? 1ull : 0ull);\n";
-    for (int v = 5; v < 64; v++)
+    for (int v = 0; v < 64; v++)
       if (used[v] && level_of(v) == 1) {
-        declare_var(v, "0u - ((tid >> " + std::to_string(v - 5 - s) + ") & 1u)", "  ");
+        declare_var(v, "0u - ((tid >> " + std::to_string(pos(v) - 5 - s) + ") & 1u)", "  ");
         st.thread_vars++;
       }
     emit_level(1, "  ");
     os << "  u64 acc = 0;\n"
        << "  for (u64 o = o_begin; o < o_end; ++o) {\n"
        << "    const u64 wo = A + (o << " << unit << ");\n";
-    for (int v = 5; v < 64; v++)
+    for (int v = 0; v < 64; v++)
       if (used[v] && level_of(v) == 2) {
-        declare_var(v, "0u - (u32)((wo >> " + std::to_string(v - 5) + ") & 1ull)", "    ");
+        declare_var(v, "0u - (u32)((wo >> " + std::to_string(pos(v) - 5) + ") & 1ull)", "    ");
         st.outer_vars++;
       }
     emit_level(2, "    ");
     os << "    u32 acc32 = 0;\n"
        << "    #pragma unroll 1\n"
        << "    for (u32 i = 0; i < " << (1u << m) << "u; ++i) {\n";
-    for (int v = 5; v < 64; v++)
+    for (int v = 0; v < 64; v++)
       if (used[v] && level_of(v) == 3) {
-        int k = v - 5 - s - t;
+        int k = pos(v) - 5 - s - t;
         declare_var(v, "(u32)(((int)(i << " + std::to_string(31 - k) + ")) >> 31)", "      ");
         st.inner_vars++;
       }

@@ -120,6 +120,8 @@ struct KernelSpec {
   int dual_pipe = 1;          // 1: balance LOP3 (ALU pipe) and IMAD (FMA pipe) cells
   int imad_cost_pct = 0;      // >0: fixed IMAD:LOP3 cost ratio (percent) instead of the sweep
   int min_blocks = 0;         // >0: __launch_bounds__ minimum resident blocks per SM
+  std::vector<int8_t> perm;   // count mode: bit position of each variable in the
+                              // word/valuation index (empty = identity)
 };
 
 struct KernelStats {
@@ -130,6 +132,15 @@ struct KernelStats {
   uint32_t inner_vars = 0, outer_vars = 0, thread_vars = 0;
   uint32_t words_per_iter = 1;
 };
+
+// Modelled time per thread-iteration of the variant's best cover.
+double model_cost(const Parsed& prog, const KernelSpec& spec);
+
+// Role search for count mode over an aligned sub-cube of 2^k_free valuations:
+// a permutation of the variables < k_free onto bit positions minimising
+// model_cost (random restarts + swap hill climbing, `budget` evaluations).
+// Returns {} when the identity is best.
+std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& spec, int k_free, int budget, uint64_t seed);
 
 // CUDA C++ source of one kernel variant (entry point "bfa_kernel").
 std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);

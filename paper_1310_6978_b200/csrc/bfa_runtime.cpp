@@ -151,6 +151,8 @@ struct Options {
   int dual_pipe = 1;
   int imad_cost_pct = 0;
   int min_blocks = 0;
+  int role_search = 1;
+  int role_budget = 200;
 };
 
 struct JitEntry {
@@ -171,6 +173,7 @@ struct bfa_prog {
   std::mutex mu;
   std::map<std::string, std::unique_ptr<JitEntry>> jit;
   std::unique_ptr<bfa::InterpProgram> interp;  // engine=1 ablation
+  std::map<std::string, std::vector<int8_t>> roles;  // role-search results
 };
 
 namespace {
@@ -179,7 +182,38 @@ std::string spec_key(const bfa::KernelSpec& s) {
   std::ostringstream k;
   k << s.mode << (s.generic ? 'g' : 's') << s.slot_bits << '.' << s.thread_bits << '.' << s.inner_bits
     << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-') << 'd' << s.dual_pipe << '.' << s.imad_cost_pct << 'b' << s.min_blocks;
+  if (!s.perm.empty()) {
+    k << 'p';
+    for (int8_t q : s.perm) k << (char)('0' + q);
+  }
   return k.str();
+}
+
+// Count mode over an aligned sub-cube of 2^k_free valuations: search (once per
+// program and variant) the variable->position permutation whose cover is
+// cheapest; the kernel then enumerates the same sub-cube in permuted order.
+void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
+  bfa_prog* p = const_cast<bfa_prog*>(cp);
+  spec->perm.clear();
+  if (!p->opt.role_search || spec->generic || spec->materialised || spec->mode != bfa::KM_COUNT || k_free < 24) return;
+  const std::string key = spec_key(*spec) + "k" + std::to_string(k_free) + "r" + std::to_string(p->opt.role_budget);
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->roles.find(key);
+    if (it != p->roles.end()) { spec->perm = it->second; return; }
+  }
+  std::vector<int8_t> perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull);
+  std::lock_guard<std::mutex> lk(p->mu);
+  p->roles[key] = perm;
+  spec->perm = perm;
+}
+
+// log2 of the valuation count if [wA, wB) (32-bit words) is an aligned
+// power-of-two sub-cube, else -1
+int aligned_k(uint64_t wA, uint64_t wB) {
+  uint64_t len = wB - wA;
+  if (!len || (len & (len - 1)) || (wA & (len - 1))) return -1;
+  return __builtin_ctzll(len) + 5;
 }
 
 // Compile (once) the variant `spec` of p; if dev >= 0 also load it on dev.
@@ -348,6 +382,7 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     spec.dual_pipe = o.dual_pipe;
     spec.imad_cost_pct = o.imad_cost_pct;
     spec.min_blocks = sg.generic ? 0 : o.min_blocks;
+    if (!sg.generic && !eval) resolve_roles(p, &spec, aligned_k(sg.wb, sg.we));
     JitEntry* je = nullptr;
     CUfunction fn;
     rc = get_kernel(p, spec, dev, &je, &fn);
@@ -382,7 +417,8 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
        << ", \"derived_outer\": " << je->stats.derived_outer << ", \"derived_inner\": " << je->stats.derived_inner
        << ", \"imad_cost\": " << je->stats.imad_cost << ", \"words_per_iter\": " << je->stats.words_per_iter
        << ", \"inner_vars\": " << je->stats.inner_vars << ", \"outer_vars\": " << je->stats.outer_vars
-       << ", \"thread_vars\": " << je->stats.thread_vars << "}";
+       << ", \"thread_vars\": " << je->stats.thread_vars
+       << ", \"roles\": \"" << (spec.perm.empty() ? "identity" : "searched") << "\"}";
   }
   js << "], \"kernels\": " << kernels << "}";
   g_last_launch = js.str();
@@ -414,6 +450,13 @@ int spec_for_what(const bfa_prog* p, int what, bfa::KernelSpec* spec) {
   spec->dual_pipe = p->opt.dual_pipe;
   spec->imad_cost_pct = p->opt.imad_cost_pct;
   spec->min_blocks = spec->generic ? 0 : p->opt.min_blocks;
+  return BFA_OK;
+}
+
+int spec_for_what_n(const bfa_prog* p, int what, int n, bfa::KernelSpec* spec) {
+  int rc = spec_for_what(p, what, spec);
+  if (rc) return rc;
+  if (what == 1 && n > 0) resolve_roles(p, spec, n);
   return BFA_OK;
 }
 
@@ -485,6 +528,8 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "dual_pipe") { if (v < 0 || v > 1) return bad(); p->opt.dual_pipe = (int)v; }
   else if (k == "imad_cost_pct") { if (v < 0 || v > 1000) return bad(); p->opt.imad_cost_pct = (int)v; }
   else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
+  else if (k == "role_search") { if (v < 0 || v > 1) return bad(); p->opt.role_search = (int)v; }
+  else if (k == "role_budget") { if (v < 1 || v > 4096) return bad(); p->opt.role_budget = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -585,7 +630,9 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
     std::vector<std::thread> th;
     std::vector<int> rcs(cands.size(), 0);
     for (size_t i = 0; i < cands.size(); i++)
-      if (ok[i]) th.emplace_back([&, i] { JitEntry* e = nullptr; rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
+      if (ok[i]) th.emplace_back([&, i] { JitEntry* e = nullptr;
+                                          resolve_roles(p, &specs[i], aligned_k(lo >> 5, hi >> 5));
+                                          rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
                                           if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner; });
     for (auto& t : th) t.join();
     for (size_t i = 0; i < cands.size(); i++)
@@ -867,14 +914,13 @@ int bfa_last_launch_json(char* buf, size_t len) {
 }
 
 int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
-  (void)n;
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   std::string s;
   if (what == 0) {
     s = bfa::dump_ir(p->parsed, nullptr);
   } else {
     bfa::KernelSpec spec;
-    int rc = spec_for_what(p, what, &spec);
+    int rc = spec_for_what_n(p, what, n, &spec);
     if (rc) return rc;
     s = bfa::emit_kernel(p->parsed, spec, nullptr);
   }
@@ -883,10 +929,9 @@ int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
 }
 
 int64_t bfa_jit_cubin(const bfa_prog* p, int what, int n, void* buf, size_t len) {
-  (void)n;
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   bfa::KernelSpec spec;
-  int rc = spec_for_what(p, what, &spec);
+  int rc = spec_for_what_n(p, what, n, &spec);
   if (rc) return rc;
   JitEntry* je = nullptr;
   rc = get_kernel(p, spec, -1, &je, nullptr);

@@ -218,6 +218,34 @@ def test_c5_bench_config_subcubes():
         assert np.array_equal(host(p.eval_range(n, lo, lo + (1 << 16))), ow)
 
 
+def test_role_search_subcubes():
+    """Count mode over an aligned sub-cube of >= 2^24 valuations enumerates it
+    in a searched variable order (DESIGN.md §5 role search): counts equal the
+    oracle's on such sub-cubes, and a program and its complement (searched
+    independently) sum to the sub-cube size."""
+    text, n, _ = W.config("c4")
+    p = bfa.Program(text)
+    refl = sum(1 << (35 - 7 * i) for i in range(6))
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        lo = (int(rng.integers(0, 1 << 36)) | refl) & ~((1 << 26) - 1)
+        assert int(p.count_range(n, lo, lo + (1 << 26)).item()) == oracle.count(text, n, lo, lo + (1 << 26))
+        assert bfa.last_launch()["segments"][0].get("roles") == "searched"
+    text, n, _ = W.config("c5")
+    p = bfa.Program(text)
+    body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+    pc = bfa.Program(f"{body}\n~{out}")
+    for lo in ((123 << 24), (1 << 42) - (1 << 24)):
+        c = int(p.count_range(n, lo, lo + (1 << 24)).item())
+        assert c == oracle.count(text, n, lo, lo + (1 << 24))
+        assert c + int(pc.count_range(n, lo, lo + (1 << 24)).item()) == 1 << 24
+    for k in (30, 36):
+        lo = (5 << 36) & ~((1 << k) - 1)
+        a = int(p.count_range(n, lo, lo + (1 << k)).item())
+        b = int(pc.count_range(n, lo, lo + (1 << k)).item())
+        assert a + b == 1 << k
+
+
 def test_autotune_keeps_results():
     """bfa_autotune only changes speed: C4 still counts 130023 and a
     sub-cube vector still equals the oracle's after tuning."""
