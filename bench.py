@@ -227,7 +227,7 @@ def run_bfa(args):
     # autotune (JIT of the candidate variants + probe timing; untimed), then
     # warm-up.  Rank 0 tunes and broadcasts its choice so every rank runs the
     # same kernel.
-    tune = prog.autotune(n) if rank == 0 else None
+    tune = prog.autotune(n, k_free=n - (world.bit_length() - 1)) if rank == 0 else None
     if world > 1:
         obj = [tune]
         dist.broadcast_object_list(obj, src=0)

@@ -109,11 +109,18 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 /* Empirical autotuning of the register-mode kernel for n variables: JIT
  * compiles a set of candidate variants (slot bits, inner-loop bits, IMAD/LOP3
  * balance) in parallel, times each on the top min(2^n, 2^36) valuations with
- * CUDA events on `stream`, and sets p's options to the fastest.  Writes a JSON
+ * CUDA events on `stream` -- each candidate with the variable roles (count
+ * mode) searched for the whole 2^n cube, as a full count would use -- and sets
+ * p's options to the fastest.  Writes a JSON
  * report (candidates, times, choice) to report (nullable).  Results do not
  * depend on the options; only speed does.  Not thread-safe with other calls on
  * the same program.  n < 24: no-op. */
 int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len);
+
+/* As bfa_autotune, for later counts over aligned sub-cubes of 2^k_free
+ * valuations (e.g. a rank's cofactor range, k_free = n - log2 P): candidates
+ * are timed with the variable roles searched for such a sub-cube. */
+int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* report, size_t len);
 
 /* ---- register-synthesised mode (generators built in registers) ---- */
 

@@ -42,6 +42,7 @@ _SIGS = {
     "bfa_dump": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t]),
     "bfa_jit_cubin": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_size_t]),
     "bfa_autotune": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_char_p, _c.c_size_t]),
+    "bfa_autotune_range": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_char_p, _c.c_size_t]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -142,10 +143,14 @@ class Program:
         _check(_load().bfa_set_option(self._h, key.encode(), int(value)))
         return self
 
-    def autotune(self, n: int, stream=None) -> dict:
-        """bfa_autotune: pick the fastest kernel variant for n (sets options)."""
+    def autotune(self, n: int, k_free: int | None = None, stream=None) -> dict:
+        """bfa_autotune(_range): pick the fastest kernel variant for counting
+        over 2^n (or aligned 2^k_free sub-cubes); sets the options."""
         buf = ctypes.create_string_buffer(1 << 16)
-        _check(_load().bfa_autotune(self._h, n, _stream(stream), buf, len(buf)))
+        if k_free is None:
+            _check(_load().bfa_autotune(self._h, n, _stream(stream), buf, len(buf)))
+        else:
+            _check(_load().bfa_autotune_range(self._h, n, k_free, _stream(stream), buf, len(buf)))
         return json.loads(buf.value.decode())
 
     # ---- register-synthesised mode

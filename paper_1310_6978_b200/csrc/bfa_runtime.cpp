@@ -296,7 +296,7 @@ std::vector<Segment> plan(const Options& o, int s, int n, uint64_t wlo, uint64_t
 
 // Common body of count_range / eval_range.
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval) {
+              cudaStream_t st, bool eval, int force_roles_k = -1) {
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
   if (p->info.max_var_id >= n)
@@ -382,7 +382,9 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     spec.dual_pipe = o.dual_pipe;
     spec.imad_cost_pct = o.imad_cost_pct;
     spec.min_blocks = sg.generic ? 0 : o.min_blocks;
-    if (!sg.generic && !eval) resolve_roles(p, &spec, aligned_k(sg.wb, sg.we));
+    // force_roles_k (autotune probes only): time the kernel whose roles were
+    // searched for a larger sub-cube; its count over this range is not used.
+    if (!sg.generic && !eval) resolve_roles(p, &spec, force_roles_k >= 0 ? force_roles_k : aligned_k(sg.wb, sg.we));
     JitEntry* je = nullptr;
     CUfunction fn;
     rc = get_kernel(p, spec, dev, &je, &fn);
@@ -566,7 +568,12 @@ int bfa_eval(const bfa_prog* p, int n, uint64_t* out) {
 }
 
 int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
+  return bfa_autotune_range(p, n, n, stream, report, len);
+}
+
+int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* report, size_t len) {
   if (!p) return set_err(BFA_E_ARG, "NULL program");
+  if (k_free < 0 || k_free > n) return set_err(BFA_E_ARG, "k_free=%d outside [0, n]", k_free);
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
   if (p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "program uses x%d >= n", p->info.max_var_id);
   int dev;
@@ -631,7 +638,7 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
     std::vector<int> rcs(cands.size(), 0);
     for (size_t i = 0; i < cands.size(); i++)
       if (ok[i]) th.emplace_back([&, i] { JitEntry* e = nullptr;
-                                          resolve_roles(p, &specs[i], aligned_k(lo >> 5, hi >> 5));
+                                          resolve_roles(p, &specs[i], k_free);
                                           rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
                                           if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner; });
     for (auto& t : th) t.join();
@@ -648,11 +655,11 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
   for (size_t i = 0; i < cands.size(); i++) {
     if (!ok[i] || cands[i].cells > 8192) continue;  // i-cache: skip very long bodies
     p->opt = cands[i].o;
-    if ((rc = run_range(p, n, lo, hi, nullptr, d, st, false))) { p->opt = base; return rc; }
+    if ((rc = run_range(p, n, lo, hi, nullptr, d, st, false, k_free))) { p->opt = base; return rc; }
     float bestms = 1e30f;
     for (int r = 0; r < 3; r++) {
       cudaEventRecord(e0, st);
-      run_range(p, n, lo, hi, nullptr, d, st, false);
+      run_range(p, n, lo, hi, nullptr, d, st, false, k_free);
       cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms = 0;
@@ -670,7 +677,7 @@ int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len) {
   cudaError_t ce = cudaStreamSynchronize(st);
   if (ce != cudaSuccess) { p->opt = base; return set_err(BFA_E_CUDA, "autotune: %s", cudaGetErrorString(ce)); }
   p->opt = best >= 0 ? cands[best].o : base;
-  js << "{\"probe_valuations\": " << (hi - lo) << ", \"candidates\": [";
+  js << "{\"probe_valuations\": " << (hi - lo) << ", \"k_free\": " << k_free << ", \"candidates\": [";
   bool first = true;
   for (size_t i = 0; i < cands.size(); i++) {
     if (cands[i].ms < 0) continue;
