@@ -16,8 +16,10 @@
  *   - a DNF vector of n variables is ceil(2^n / 64) (at least 1) little-endian
  *     uint64 words; bit mu lives in word mu >> 6 at bit mu & 63.  For n < 6
  *     the unused high bits of word 0 are 0.
- *   - 0 <= n <= 63; every variable id used by the program must be < n;
- *     unused ids < n are free (each doubles the count).
+ *   - 0 <= n <= 63 for evaluation (counts are uint64); every variable id used
+ *     by the program must be < n; unused ids < n are free (each doubles the
+ *     count).  Programs may use ids up to 63 (e.g. 8 x 8 relation letters) and
+ *     be reduced below 64 variables with bfa_assume (n = 64 allowed there).
  *
  * Expression grammar (UTF-8 text; the compiler and the CPU oracle implement it
  * independently):
@@ -31,7 +33,7 @@
  *   xor     := and { '^' and }                       XOR is the paper's '+'
  *   and     := unary { '&' unary }
  *   unary   := '~' unary | atom
- *   atom    := 'x'DIGITS (id <= 62) | '0' | '1' | NAME | '(' expr ')'
+ *   atom    := 'x'DIGITS (id <= 63) | '0' | '1' | NAME | '(' expr ')'
  *   Newlines inside parentheses are whitespace.  The program's value is the
  *   conjunction of all constraint statements (a system e_i = phi_i is solved
  *   when every phi_i = 1); no constraints -> constant 1.
@@ -146,6 +148,29 @@ int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
  * there. */
 int bfa_eval_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
                    uint64_t* out_dev, uint64_t* count_dev, void* stream);
+
+/* ---- killing variables and model enumeration ---- */
+
+/* Killing variables (§3.3; the `assumptions` of §4.2,
+ * PAPER.md:1104-1125): variables v < n with bit v of `mask` set are fixed to
+ * bit v of `values`, the Reduction is re-run, and the remaining variables
+ * < n are renumbered densely in increasing order.  *out is a new program over
+ * *n_free = n - popcount(mask & (2^n - 1)) variables (its own options are
+ * copied from p); free_ids (nullable, >= n entries) receives the original id
+ * of each new id, so a model mu' of *out is the model
+ * deposit(mu', free_ids) | (values & mask) of p. */
+int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_prog** out, int* n_free,
+               int* free_ids);  /* 0 <= n <= 64 */
+
+/* Model enumeration ("all labeled models"; out.txt rows,
+ * PAPER.md:1091-1096): the models mu in [mu_lo, mu_hi) (bounds as for
+ * bfa_count_range), ascending, into the device list mu_out (capacity
+ * entries).  *count_dev (device) receives the total number of models; if it
+ * exceeds capacity the list holds an unspecified subset of them.  Meant for
+ * sparse results (each model is appended with one atomic per word).
+ * Synchronous on `stream`. */
+int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* mu_out, uint64_t capacity,
+                  uint64_t* count_dev, void* stream);
 
 /* ---- materialised mode (the paper's vector formulation) ---- */
 

@@ -186,7 +186,7 @@ static int p_atom(Lex* L, OProg* P) {
   if (L->failed) return -1;
   switch (L->tok) {
     case T_VAR: {
-      if (L->ival > 62) { lex_error(L, "variable id %lld > 62", L->ival); return -1; }
+      if (L->ival > 63) { lex_error(L, "variable id %lld > 63", L->ival); return -1; }
       int id = (int)L->ival;
       if (id > P->max_var) P->max_var = id;
       next(L);

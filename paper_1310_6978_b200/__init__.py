@@ -13,7 +13,7 @@ import ctypes
 import json
 import os
 
-__all__ = ["Program", "BfaError", "words_for", "last_launch", "fill_generators", "popcount",
+__all__ = ["Program", "BfaError", "words_for", "reinstate", "last_launch", "fill_generators", "popcount",
            "peak_int", "lib_path", "version"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -43,6 +43,10 @@ _SIGS = {
     "bfa_jit_cubin": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_size_t]),
     "bfa_autotune": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_void_p, _c.c_char_p, _c.c_size_t]),
     "bfa_autotune_range": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_void_p, _c.c_char_p, _c.c_size_t]),
+    "bfa_assume": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.POINTER(_c.c_void_p),
+                              _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
+    "bfa_enumerate": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_uint64,
+                                 _c.c_void_p, _c.c_void_p]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -180,6 +184,36 @@ class Program:
         _check(_load().bfa_eval_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), cp, _stream(stream)))
         return out
 
+    # ---- killing variables / enumeration
+    def assume(self, n: int, assignment: dict):
+        """bfa_assume: fix variables (id -> 0/1), re-run the Reduction and
+        renumber the free variables densely.  Returns (program, n_free,
+        free_ids) with free_ids[new id] = original id."""
+        mask = values = 0
+        for v, b in assignment.items():
+            mask |= 1 << v
+            values |= (1 << v) if b else 0
+        h = ctypes.c_void_p()
+        nf = ctypes.c_int()
+        ids = (ctypes.c_int * 64)()
+        _check(_load().bfa_assume(self._h, n, mask, values, ctypes.byref(h), ctypes.byref(nf), ids))
+        q = Program.__new__(Program)
+        q._h = h
+        q.text = None
+        return q, nf.value, list(ids[:nf.value])
+
+    def enumerate(self, n: int, lo: int = 0, hi: int | None = None, capacity: int = 1 << 20, stream=None):
+        """bfa_enumerate: ascending models in [lo, hi) as a device int64 tensor
+        (at most `capacity`), and the total number of models."""
+        import torch
+        hi = (1 << n) if hi is None else hi
+        out = torch.empty(max(capacity, 1), dtype=torch.int64, device="cuda")
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        _check(_load().bfa_enumerate(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), capacity,
+                                     ctypes.c_void_p(cnt.data_ptr()), _stream(stream)))
+        total = int(cnt.item())
+        return out[:min(total, capacity)], total
+
     # ---- materialised mode
     def eval_materialised(self, n: int, variant: int = 0, out=None, count_out=None, stream=None):
         out = _u64_out(out, words_for(n))
@@ -202,6 +236,20 @@ class Program:
         buf = ctypes.create_string_buffer(size)
         _check(lib.bfa_jit_cubin(self._h, what, n, buf, size))
         return buf.raw
+
+
+def reinstate(mu_free, free_ids, assignment: dict) -> list:
+    """Map models of an assumed program back to valuations of the original
+    (killed letters reinstated)."""
+    fixed = sum((1 << v) for v, b in assignment.items() if b)
+    out = []
+    for m in mu_free:
+        m = int(m)
+        full = fixed
+        for new, old in enumerate(free_ids):
+            full |= ((m >> new) & 1) << old
+        out.append(full)
+    return out
 
 
 def _err_code() -> int:

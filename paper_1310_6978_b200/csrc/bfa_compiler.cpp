@@ -199,7 +199,7 @@ struct Parser {
     Dag& d = P->dag;
     switch (lx.tok) {
       case VAR: {
-        if (lx.ival > 62) { lx.fail("variable id " + std::to_string(lx.ival) + " > 62"); return 0; }
+        if (lx.ival > 63) { lx.fail("variable id " + std::to_string(lx.ival) + " > 63"); return 0; }
         int id = (int)lx.ival;
         P->max_var = std::max(P->max_var, id);
         P->support_mask |= 1ull << id;
@@ -367,6 +367,38 @@ static Lit rebuild(const Dag& src, Lit root, const std::vector<Lit>& subst, Dag&
     stack.pop_back();
   }
   return memo[lit_node(root)] ^ (root & 1u);
+}
+
+Parsed assume(const Parsed& src, int n, uint64_t mask, uint64_t values, std::vector<int>* free_ids) {
+  Parsed out;
+  out.tree_nodes = src.tree_nodes;
+  out.lets = src.lets;
+  std::vector<Lit> subst(64, 0);
+  std::vector<int> ids;
+  for (int v = 0; v < 64; v++) {
+    if (v < n && ((mask >> v) & 1)) {
+      subst[v] = ((values >> v) & 1) ? out.dag.const1() : out.dag.const0();
+    } else {
+      subst[v] = out.dag.var((uint32_t)ids.size());
+      if (v < n) ids.push_back(v);
+    }
+  }
+  std::vector<uint8_t> done(src.dag.nodes.size(), 0);
+  std::vector<Lit> memo(src.dag.nodes.size(), 0);
+  out.root = rebuild(src.dag, src.root, subst, out.dag, memo, done);
+  // support of the reduced program
+  std::vector<uint8_t> seen(out.dag.nodes.size(), 0);
+  std::vector<uint32_t> st{lit_node(out.root)};
+  while (!st.empty()) {
+    uint32_t k = st.back(); st.pop_back();
+    if (seen[k]) continue;
+    seen[k] = 1;
+    const Node& nd = out.dag.nodes[k];
+    if (nd.kind == NK_GATE) { st.push_back(nd.a); st.push_back(nd.b); }
+    if (nd.kind == NK_VAR) { out.support_mask |= 1ull << nd.val; out.max_var = std::max(out.max_var, (int)nd.val); }
+  }
+  if (free_ids) *free_ids = ids;
+  return out;
 }
 
 // ============================================================== LUT3 mapping
@@ -663,6 +695,17 @@ const char* kPrelude =
     "typedef unsigned long long u64;\n"
     "struct __align__(16) u32x4 { u32 x, y, z, w; };\n"
     "struct __align__(8) u32x2 { u32 x, y; };\n"
+    "// enumerate mode: append the valuations of the set bits of word w\n"
+    "__device__ __forceinline__ void bfa_append(u32 r, u64 w, u64* cursor, u64* mu_out, u64 cap) {\n"
+    "  if (!r) return;\n"
+    "  u64 pos = atomicAdd(cursor, (u64)__popc(r));\n"
+    "  while (r) {\n"
+    "    const int j = __ffs(r) - 1;\n"
+    "    r &= r - 1u;\n"
+    "    if (pos < cap) mu_out[pos] = (w << 5) | (u64)j;\n"
+    "    ++pos;\n"
+    "  }\n"
+    "}\n"
     "__device__ __forceinline__ void bfa_block_sum(u64 acc, u64* count) {\n"
     "  #pragma unroll\n"
     "  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
@@ -841,6 +884,8 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   const std::vector<Lit>& outs = b.outs;
   const int S = b.S, s = b.s, t = b.t, m = b.m;
   const bool want_count = spec.mode == KM_COUNT || spec.fuse_count;
+  const bool enumerate = spec.mode == KM_ENUM;
+  const std::string enum_params = enumerate ? ", u64* __restrict__ mu_out, const u64 cap" : "";
   auto level_of = [&](int v) { return (int)b.var_level[v]; };
   auto pos = [&](int v) { return b.pos[v]; };
   double best_t = 0;
@@ -908,7 +953,8 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     for (int v = 0; v < 64; v++) st.inner_vars += used[v];
   } else if (spec.generic) {
     os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
-       << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ out, u64* __restrict__ count"
+       << enum_params << ") {\n"
        << "  u64 acc = 0;\n"
        << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
        << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += stride) {\n"
@@ -918,6 +964,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     emit_level(3, "    ");
     os << "    const u32 r = (" << E.value(outs[0]) << ") & mask;\n";
     if (spec.mode == KM_EVAL) os << "    out[k] = r;\n";
+    if (enumerate) os << "    bfa_append(r, w, count, mu_out, cap);\n";
     if (want_count) os << "    acc += __popc(r);\n";
     os << "  }\n";
     if (want_count) os << "  bfa_block_sum(acc, count);\n";
@@ -927,7 +974,8 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   } else {
     const int unit = s + t + m;
     os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
-       << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
+       << enum_params << ") {\n"
        << "  const u32 tid = threadIdx.x;\n"
        << "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n"
        << "  const u64 o_begin = b * q + (b < rr ? b : rr);\n"
@@ -966,6 +1014,10 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
         for (int g = 0; g < S; g += 4)
           os << "      *reinterpret_cast<u32x4*>(out + idx + " << g << ") = u32x4{r" << g << ", r" << g + 1
              << ", r" << g + 2 << ", r" << g + 3 << "};\n";
+    }
+    if (enumerate) {
+      os << "      const u64 wbase = wo + ((u64)i << " << (s + t) << ") + ((u64)tid << " << s << ");\n";
+      for (int sl = 0; sl < S; sl++) os << "      bfa_append(r" << sl << ", wbase + " << sl << ", count, mu_out, cap);\n";
     }
     if (want_count) {
       os << "      acc32 += ";

@@ -78,6 +78,13 @@ struct Parsed {
 // Parse `text` (grammar in include/bfa.h).  Returns 0 or -1 with "line:col: msg".
 int parse_program(const std::string& text, Parsed* out, std::string* err);
 
+// Killing variables (§3.3; the `assumptions` of §4.2,
+// PAPER.md:1104-1125): variables v < n with bit v of `mask` set become the
+// constant bit v of `values`; the Reduction runs again; the surviving
+// variables < n are renumbered densely in increasing order.  free_ids[new] =
+// old id.
+Parsed assume(const Parsed& src, int n, uint64_t mask, uint64_t values, std::vector<int>* free_ids);
+
 // ---------------------------------------------------------------- mapping
 struct Lut {
   uint32_t root;      // node id in the mapped DAG
@@ -106,7 +113,7 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
                    double imad_cost = 0.0);
 
 // ---------------------------------------------------------------- kernels
-enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1 };
+enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1, KM_ENUM = 2 };
 
 struct KernelSpec {
   KernelMode mode = KM_COUNT;

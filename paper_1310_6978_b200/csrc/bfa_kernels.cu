@@ -7,6 +7,7 @@
 //   peak_lop3  : LOP3 issue-rate microbenchmark (the int-ALU denominator)
 // The register-mode kernels are generated per program and JIT-compiled
 // (bfa_compiler.cpp / bfa_runtime.cpp).
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -292,6 +293,23 @@ cudaError_t interp(const uint32_t* ops, int n_ops, const uint32_t* consts, int n
   e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the symbol may be rewritten after we return
   if (block_used) *block_used = T;
+  return e;
+}
+
+cudaError_t sort_u64(uint64_t* keys, uint64_t n, int end_bit, cudaStream_t st) {
+  size_t temp = 0;
+  unsigned long long* k = reinterpret_cast<unsigned long long*>(keys);
+  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, temp, k, k, (int64_t)n, 0, end_bit, st);
+  if (e != cudaSuccess) return e;
+  unsigned long long* alt = nullptr;
+  void* tmp = nullptr;
+  if ((e = cudaMallocAsync(&alt, n * 8, st)) != cudaSuccess) return e;
+  if ((e = cudaMallocAsync(&tmp, temp, st)) != cudaSuccess) { cudaFreeAsync(alt, st); return e; }
+  cub::DoubleBuffer<unsigned long long> db(k, alt);
+  e = cub::DeviceRadixSort::SortKeys(tmp, temp, db, (int64_t)n, 0, end_bit, st);
+  if (e == cudaSuccess && db.Current() != k) e = cudaMemcpyAsync(k, db.Current(), n * 8, cudaMemcpyDeviceToDevice, st);
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(alt, st);
   return e;
 }
 

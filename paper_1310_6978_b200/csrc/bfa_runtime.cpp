@@ -296,7 +296,8 @@ std::vector<Segment> plan(const Options& o, int s, int n, uint64_t wlo, uint64_t
 
 // Common body of count_range / eval_range.
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval, int force_roles_k = -1) {
+              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
+  const bool enumerate = mu_out != nullptr;
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
   if (p->info.max_var_id >= n)
@@ -311,6 +312,7 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
                    (unsigned long long)align);
   if (eval && !out_dev) return set_err(BFA_E_ARG, "NULL output buffer");
   if (!eval && !count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
+  if (enumerate && (eval || p->opt.engine == 1)) return set_err(BFA_E_ARG, "enumerate: JIT count path only");
   int dev;
   DevInfo di;
   int rc = current_device(&dev, &di);
@@ -373,7 +375,7 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   for (size_t k = 0; k < segs.size(); k++) {
     const Segment& sg = segs[k];
     bfa::KernelSpec spec;
-    spec.mode = eval ? bfa::KM_EVAL : bfa::KM_COUNT;
+    spec.mode = eval ? bfa::KM_EVAL : enumerate ? bfa::KM_ENUM : bfa::KM_COUNT;
     spec.generic = sg.generic;
     spec.slot_bits = sg.generic ? 0 : s_eff;
     spec.thread_bits = o.thread_bits;
@@ -397,14 +399,14 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
       uint64_t wb = sg.wb, wc = sg.we - sg.wb;
       uint32_t* o32 = eval ? out32 + (sg.wb - wlo) : nullptr;
       grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((wc + T - 1) / T, grid_cap));
-      void* args[] = {&wb, &wc, &mask, &o32, &cnt};
+      void* args[] = {&wb, &wc, &mask, &o32, &cnt, &mu_out, &cap};
       rc = launch(fn, grid, T, st, args);
     } else {
       const int ub = s_eff + o.thread_bits + sg.m;
       uint64_t A = sg.wb, O = (sg.we - sg.wb) >> ub, base = wlo;
       uint32_t* o32 = out32;
       grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(O, grid_cap));
-      void* args[] = {&A, &O, &base, &o32, &cnt};
+      void* args[] = {&A, &O, &base, &o32, &cnt, &mu_out, &cap};
       rc = launch(fn, grid, T, st, args);
     }
     if (rc) return rc;
@@ -471,11 +473,7 @@ extern "C" {
 const char* bfa_last_error(void) { return g_err.c_str(); }
 const char* bfa_version(void) { return "bfa 0.1 (sm_100a; NVRTC static)"; }
 
-int bfa_compile(const char* expr, bfa_prog** out) {
-  if (!expr || !out) return set_err(BFA_E_ARG, "NULL argument");
-  auto p = std::make_unique<bfa_prog>();
-  std::string err;
-  if (bfa::parse_program(expr, &p->parsed, &err) != 0) return set_err(BFA_E_PARSE, "%s", err.c_str());
+static void fill_info(bfa_prog* p) {
   bfa_info& I = p->info;
   const bfa::Parsed& P = p->parsed;
   I.max_var_id = P.max_var;
@@ -504,7 +502,62 @@ int bfa_compile(const char* expr, bfa_prog** out) {
     bfa::dump_ir(P, &L);
     I.luts = L;
   }
+}
+
+int bfa_compile(const char* expr, bfa_prog** out) {
+  if (!expr || !out) return set_err(BFA_E_ARG, "NULL argument");
+  auto p = std::make_unique<bfa_prog>();
+  std::string err;
+  if (bfa::parse_program(expr, &p->parsed, &err) != 0) return set_err(BFA_E_PARSE, "%s", err.c_str());
+  fill_info(p.get());
   *out = p.release();
+  return BFA_OK;
+}
+
+int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_prog** out, int* n_free,
+               int* free_ids) {
+  if (!p || !out) return set_err(BFA_E_ARG, "NULL argument");
+  if (n < 0 || n > 64) return set_err(BFA_E_RANGE, "n=%d outside [0, 64]", n);
+  if (p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "program uses x%d >= n", p->info.max_var_id);
+  auto q = std::make_unique<bfa_prog>();
+  std::vector<int> ids;
+  q->parsed = bfa::assume(p->parsed, n, mask, values, &ids);
+  q->opt = p->opt;
+  fill_info(q.get());
+  if (n_free) *n_free = (int)ids.size();
+  if (free_ids) for (size_t i = 0; i < ids.size(); i++) free_ids[i] = ids[i];
+  *out = q.release();
+  return BFA_OK;
+}
+
+int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* mu_out, uint64_t capacity,
+                  uint64_t* count_dev, void* stream) {
+  if (!mu_out && capacity) return set_err(BFA_E_ARG, "NULL output list");
+  if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  uint64_t dummy_cap = capacity;
+  uint64_t* list = mu_out;
+  uint64_t* scratch = nullptr;
+  if (!list) {  // count-only call still needs a valid pointer
+    if (cudaMallocAsync(&scratch, 8, st) != cudaSuccess) return set_err(BFA_E_NOMEM, "cudaMallocAsync");
+    list = scratch;
+    dummy_cap = 0;
+  }
+  int rc = run_range(p, n, mu_lo, mu_hi, nullptr, count_dev, st, false, -1, list, dummy_cap);
+  if (rc) { if (scratch) cudaFreeAsync(scratch, st); return rc; }
+  uint64_t found = 0;
+  cudaError_t e = cudaMemcpyAsync(&found, count_dev, 8, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (scratch) cudaFreeAsync(scratch, st);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "enumerate: %s", cudaGetErrorString(e));
+  const uint64_t m = std::min(found, capacity);
+  if (m > 1) {
+    int bits = 1;
+    while (bits < 64 && (mu_hi - 1) >> bits) bits++;
+    e = bfa_k::sort_u64(list, m, bits, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_err(BFA_E_CUDA, "enumerate sort: %s", cudaGetErrorString(e));
+  }
   return BFA_OK;
 }
 

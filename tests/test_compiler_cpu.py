@@ -113,7 +113,7 @@ def test_reduction_and_info():
     assert c4["support"] == 36 and c4["luts"] <= c4["gates"]
 
 
-@pytest.mark.parametrize("bad", ["x0 &", "(x0", "x0 x1", "2", "x63", "y", "let a = x0\nlet a = x1",
+@pytest.mark.parametrize("bad", ["x0 &", "(x0", "x0 x1", "2", "x64", "y", "let a = x0\nlet a = x1",
                                  "x0 $ x1", "let = x0", "a = x0\na = x1"])
 def test_parse_errors_agree_with_oracle(bad):
     with pytest.raises(bfa.BfaError) as e:
@@ -154,3 +154,41 @@ def test_no_cpu_fallback():
     with pytest.raises(bfa.BfaError) as e:
         p.count(9)
     assert e.value.code == bfa.BFA_E_CUDA
+
+
+# ----------------------------------------------------------- killing variables
+def test_bounded_poset_kill_counts():
+    """PAPER.md:1193-1203 (§5.2, Eq. conspa, reading C-13): 5k-6 letters are
+    killed, leaving v = k^2 - 5k + 6 (v = 30 at k = 8); the kills never
+    assign one letter two values."""
+    for k in range(2, 11):
+        a = W.bounded_poset_kills(k)
+        assert len(a) == 5 * k - 6
+        assert k * k - len(a) == k * k - 5 * k + 6
+    assert 64 - len(W.bounded_poset_kills(8)) == 30
+
+
+def test_assume_matches_oracle():
+    """bfa_assume = substitute + Reduction + dense renumbering: the reduced
+    program's LUT cover, evaluated here over the free letters, equals the
+    oracle's models of the original program with the kills as conjuncts
+    (each mapped to its free bits)."""
+    for gen, k in ((W.posets, 4), (W.posets, 5), (W.equivalences, 4)):
+        text = gen(k)
+        a = W.bounded_poset_kills(k)
+        q, nf, ids = bfa.Program(text).assume(k * k, a)
+        assert nf == k * k - len(a) and ids == sorted(set(range(k * k)) - set(a))
+        lits = "\n".join(("" if b else "~") + f"x{v}" for v, b in a.items())
+        ow, oc = oracle.evaluate(text + lits + "\n", k * k)
+        full = oracle.set_bits(ow)
+        reduced = sorted(sum(((int(m) >> old) & 1) << new for new, old in enumerate(ids)) for m in full)
+        tt = eval_ir(q.dump(0), nf)
+        assert [int(x) for x in np.nonzero(tt)[0]] == reduced
+        assert q.info["max_var_id"] < nf
+
+
+def test_assume_to_constant():
+    q, nf, ids = bfa.Program("x0 & x5 | x3").assume(6, {0: 1, 5: 1})
+    assert q.info["const_value"] == 1 and nf == 4 and ids == [1, 2, 3, 4]
+    q, nf, _ = bfa.Program("x63 & x1").assume(64, {63: 0})
+    assert q.info["const_value"] == 0 and nf == 63

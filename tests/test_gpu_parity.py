@@ -259,6 +259,82 @@ def test_autotune_keeps_results():
     assert np.array_equal(host(p.eval_range(n, lo, 1 << 36)), ow)
 
 
+# ------------------------------------------------------------ NEXT-1 / NEXT-2
+def test_bounded_posets_n8_paper():
+    """PAPER.md:1193-1204 (§5.2): bounded posets on 8 points; killing 34
+    letters (Eq. conspa) leaves v = 30, whose models are the partial orders
+    of the 6 middle elements: |K| = A001035(6) = 130023, and
+    l_{T,8} = 8 * 7 * |K| = 7,281,288.  Enumerated models, reinstated,
+    satisfy the unreduced theory (checked by the oracle for k = 7)."""
+    k = 8
+    a = W.bounded_poset_kills(k)
+    q, nf, ids = bfa.Program(W.posets(k)).assume(64, a)
+    assert nf == 30
+    c = q.count(nf)
+    assert c == 130023 and k * (k - 1) * c == 7281288
+    mus, total = q.enumerate(nf, capacity=1 << 18)
+    assert total == 130023 and len(mus) == total
+    m = mus.cpu().numpy()
+    assert (np.diff(m) > 0).all()
+    k = 7
+    text = W.posets(k)
+    a = W.bounded_poset_kills(k)
+    q, nf, ids = bfa.Program(text).assume(49, a)
+    mus, total = q.enumerate(nf, capacity=1 << 16)
+    assert total == 4231                       # A001035(5)
+    full = bfa.reinstate(mus.cpu().numpy()[::97], ids, a)
+    for mu in full:
+        assert oracle.count(text, 49, mu, mu + 1) == 1
+
+
+def test_special_posets_assumptions():
+    """SO.txt with assumptions p(i,i) = 1: k = 5 gives
+    the closed form 1840 (SURVEY P-9) on 20 free letters; k = 6 is the paper's
+    run with 30 unknowns, checked against the oracle on
+    the reduced program's text."""
+    import re
+    for k, expect in ((5, 1840), (6, None)):
+        text = W.special_posets(k)
+        a = {W.letter_id(k, i, i): 1 for i in range(k)}
+        q, nf, ids = bfa.Program(text).assume(k * k, a)
+        assert nf == k * k - k
+        c = q.count(nf)
+        if expect is not None:
+            assert c == expect
+        else:
+            # the reduced program as text (test-side substitution + renumbering)
+            new = {old: i for i, old in enumerate(ids)}
+            red = re.sub(r"\bx(\d+)\b", lambda mm: str(a[int(mm.group(1))]) if int(mm.group(1)) in a
+                         else f"x{new[int(mm.group(1))]}", text)
+            assert c == oracle.count(red, nf)
+
+
+def test_enumerate_matches_oracle(golden):
+    g = golden("c1_posets3.json")
+    mus, total = bfa.Program(W.posets(3)).enumerate(9)
+    assert total == 19 and mus.cpu().tolist() == g["set_bits"]
+    mus, total = bfa.Program(W.BAEQU).enumerate(4)
+    assert mus.cpu().tolist() == [0, 9, 15]
+    text, n, _ = W.config("c3_posets")
+    ow, oc = oracle.evaluate(text, n)
+    mus, total = bfa.Program(text).enumerate(n, capacity=8192)
+    assert total == oc == 4231 and np.array_equal(mus.cpu().numpy(), oracle.set_bits(ow))
+    for seed in (7, 17, 27, 37):
+        p = W.random_program(seed, max_n=20)
+        ow, oc = oracle.evaluate(p.text, p.n)
+        mus, total = bfa.Program(p.text).enumerate(p.n, capacity=1 << 21)
+        assert total == oc and np.array_equal(mus.cpu().numpy(), oracle.set_bits(ow))
+    # a sub-range of C4 and a too-small capacity (count still exact)
+    text, n, _ = W.config("c4")
+    refl = sum(1 << (35 - 7 * i) for i in range(6))
+    lo = refl & ~((1 << 24) - 1)
+    ow, oc = oracle.evaluate(text, n, lo, lo + (1 << 24))
+    mus, total = bfa.Program(text).enumerate(n, lo, lo + (1 << 24), capacity=1 << 16)
+    assert total == oc and np.array_equal(mus.cpu().numpy(), oracle.set_bits(ow, lo))
+    _, total = bfa.Program(text).enumerate(n, capacity=4)
+    assert total == 130023
+
+
 # ------------------------------------------------------------ materialised mode
 def test_fill_generators_and_popcount():
     n = 12

@@ -148,7 +148,7 @@ def test_hand_tables_are_what_they_say():
     assert tt_bits(3, lambda a, b, c: a == ((not b) or c)) == HAND[7][2]
 
 
-@pytest.mark.parametrize("bad", ["x0 &", "(x0", "x0 x1", "2", "x63", "y", "let a = x0\nlet a = x1",
+@pytest.mark.parametrize("bad", ["x0 &", "(x0", "x0 x1", "2", "x64", "y", "let a = x0\nlet a = x1",
                                  "x0 $ x1", "let = x0", "a = x0\na = x1"])
 def test_parse_errors(bad):
     with pytest.raises(oracle.OracleError) as e:

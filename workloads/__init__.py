@@ -105,6 +105,23 @@ def bounded_posets(k: int) -> str:
     return _program(_refl(k) + _antisym(k) + _trans(k) + [least, great])
 
 
+def bounded_poset_kills(k: int) -> dict:
+    """Eq. (conspa) of PAPER.md:1194-1198 (reading C-13: p_{0i} = 1,
+    p_{j0} = 0, p_{i,k-1} = 1, p_{k-1,j} = 0, p_{ii} = 1): the assumptions
+    that make 0 the least and k-1 the greatest element.  5k-6 letters are
+    killed, leaving v = k^2 - 5k + 6."""
+    a = {}
+    for i in range(k):
+        a[letter_id(k, 0, i)] = 1
+        a[letter_id(k, i, k - 1)] = 1
+        a[letter_id(k, i, i)] = 1
+    for j in range(1, k):
+        a[letter_id(k, j, 0)] = 0
+    for j in range(0, k - 1):
+        a[letter_id(k, k - 1, j)] = 0
+    return a
+
+
 # BAequ (PAPER.md:1154-1165, §5.1) with x=id3, y=id2, z=id1, u=id0 (reading C-1)
 BAEQU = "e1 = x3 ^ x2 ^ ~x1 ^ x0\ne2 = ~((x3 | x2 & x1) ^ x0)\n"
 
