@@ -64,6 +64,8 @@ CONFIG_DESC = {
     "c4": "labeled partial orders on 6 points, n=36, count mode (BASELINE configs[3])",
     "c3_posets": "labeled partial orders on 5 points, n=25, count mode (BASELINE configs[2])",
     "c3_equiv": "equivalence relations on 5 points, n=25, count mode (BASELINE configs[2])",
+    "paper_2p17": "the paper's timed experiment shape: a 30-variable term with 2^17 tree nodes, all 2^30 valuations "
+                  "(PAPER.md:374-380; ~1 s on the paper's 2-GPU rig), segmented execution",
 }
 
 
@@ -232,7 +234,7 @@ def run_bfa(args):
         obj = [tune]
         dist.broadcast_object_list(obj, src=0)
         tune = obj[0]
-    for key, val in (tune.get("best") or {}).items():
+    for key, val in ((tune or {}).get("best") or {}).items():
         prog.set_option(key, val)
     for _ in range(max(args.warmup, 3)):
         step()
@@ -286,10 +288,14 @@ def run_bfa(args):
     # program is the cell cover of f cofactored on the slot variables, with
     # loop-invariant cells hoisted: LOP3 cells on the ALU pipe,
     # IMAD cells (+ their operand registers) on the FMA pipe.
-    seg = max(launch["segments"], key=lambda g: g["words"])
-    S, m = seg["words_per_iter"], seg["m"]
-    lop3_w = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
-    imad_w = (seg["imads_inner"] + seg["derived_inner"]) / S + (seg["imads_outer"] + seg["derived_outer"]) / (S << m)
+    if launch.get("variant") == "segmented":      # NEXT-3: every cell per word, LOP3 only
+        lop3_w, imad_w = launch["cells"] / 1.0, 0.0
+        lop3_w = launch.get("emitted", launch["cells"])
+    else:
+        seg = max(launch["segments"], key=lambda g: g["words"])
+        S, m = seg["words_per_iter"], seg["m"]
+        lop3_w = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
+        imad_w = (seg["imads_inner"] + seg["derived_inner"]) / S + (seg["imads_outer"] + seg["derived_outer"]) / (S << m)
     cells_w = lop3_w + imad_w
     achieved = cells_w * words_per_launch / kernel_s           # integer cell ops/s per GPU
     sm_clock = clk["sm_max_mhz"] or 1965.0

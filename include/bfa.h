@@ -105,6 +105,14 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "imad_cost_pct" IMAD:LOP3 cost ratio in percent for that mapping, 0 = model
  *                   sweep (default 0)
  *   "min_blocks"    __launch_bounds__ minimum blocks per SM, 0 = none (default 0)
+ *   "role_search"   1 = count mode searches the variable -> bit-position roles on
+ *                   aligned sub-cubes of >= 2^24 valuations (default 1)
+ *   "role_budget"   model evaluations of that search (default 200)
+ *   "segment_cells" programs whose cover exceeds 8000 LUTs run as segments of
+ *                   this many cells (0 = auto: 768), values crossing segments in
+ *                   HBM slot arrays
+ *   "segment_remat" recompute shared cells whose cone has <= this many cells in
+ *                   each segment instead of storing them (default 2)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 
@@ -212,6 +220,9 @@ int bfa_last_launch_json(char* buf, size_t len);
  * what = 1: CUDA source of the specialised count kernel for n.
  * what = 2: CUDA source of the specialised eval kernel for n.
  * what = 3: CUDA source of the unspecialised (generic) count kernel.
+ * what = 4: CUDA source of the fused materialised-mode kernel.
+ * what = 5: JSON summary of the segmented-execution plan (large programs).
+ * what = 6: CUDA source of segment n of that plan.
  * Returns the full length needed (excluding NUL) or a negative error. */
 int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len);
 

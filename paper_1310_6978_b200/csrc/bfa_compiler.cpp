@@ -618,6 +618,7 @@ struct Emitter {
   }
   // IMAD operand registers: (u, k, c) -> u * k + c, computed once at u's level
   std::map<uint32_t, std::set<std::pair<int, int>>> derived;
+  uint64_t cells_emitted = 0;
 
   static void mc(uint8_t f, int* m, int* c) {  // unary f(x) = x * m + c
     switch (f) {
@@ -661,6 +662,7 @@ struct Emitter {
          << " + " << imm(kc.second) << ";\n";
   }
   void lut(const Lut& L, const char* indent) {
+    cells_emitted++;
     if (L.kind == 1) {
       // u ? f1(x) : f0(x) = x * M + C with M = m0 + (m0 - m1) u, C = c0 + (c0 - c1) u
       // (u is 0 or ~0 = -1 in every word)
@@ -821,6 +823,39 @@ static MapResult choose_mapping(const Built& b, const KernelSpec& spec, double* 
   return mr;
 }
 
+// Emission order: depth-first post-order from the outputs (slot by slot), so
+// a subtree is finished before the next starts and live ranges stay short;
+// node-id order would keep e.g. every shared subterm of a big tree alive.
+static void dfs_order(MapResult* mr, const std::vector<Lit>& outs) {
+  std::unordered_map<uint32_t, size_t> at;
+  for (size_t k = 0; k < mr->luts.size(); k++) at[mr->luts[k].root] = k;
+  std::vector<uint8_t> done(mr->luts.size(), 0);
+  std::vector<Lut> order;
+  order.reserve(mr->luts.size());
+  for (Lit o : outs) {
+    auto r = at.find(lit_node(o));
+    if (r == at.end()) continue;
+    std::vector<std::pair<size_t, int>> st{{r->second, 0}};
+    while (!st.empty()) {
+      size_t k = st.back().first;
+      int q = st.back().second;
+      if (done[k]) { st.pop_back(); continue; }
+      const Lut& L = mr->luts[k];
+      const int nin = L.kind == 1 ? 2 : L.nin;
+      if (q < nin) {
+        st.back().second++;
+        auto it = at.find(L.in[q]);
+        if (it != at.end() && !done[it->second]) st.push_back({it->second, 0});
+        continue;
+      }
+      done[k] = 1;
+      order.push_back(L);
+      st.pop_back();
+    }
+  }
+  mr->luts.swap(order);
+}
+
 double model_cost(const Parsed& prog, const KernelSpec& spec) {
   Built b;
   build_specialised(prog, spec, &b);
@@ -890,6 +925,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   auto pos = [&](int v) { return b.pos[v]; };
   double best_t = 0;
   MapResult mr = choose_mapping(b, spec, &best_t, &st.imad_cost);
+  dfs_order(&mr, outs);
 
   // which variables are referenced (as cell inputs or outputs)
   std::vector<uint8_t> used(64, 0);
@@ -1033,6 +1069,146 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   }
   if (stats) *stats = st;
   return os.str();
+}
+
+SegPlan emit_segmented(const Parsed& prog, KernelMode mode, bool fuse_count, int seg_cells, int thread_bits,
+                       int imad_cost_pct, int remat_cells) {
+  KernelSpec spec;
+  spec.mode = mode;
+  spec.generic = true;
+  spec.slot_bits = 0;
+  spec.thread_bits = thread_bits;
+  spec.inner_bits = 0;
+  spec.dual_pipe = imad_cost_pct > 0;
+  spec.imad_cost_pct = imad_cost_pct;
+  Built b;
+  build_specialised(prog, spec, &b);
+  const Dag& D = b.D;
+  MapResult mr = choose_mapping(b, spec, nullptr, nullptr);
+  dfs_order(&mr, b.outs);
+  const size_t C = mr.luts.size();
+  SegPlan plan;
+  const int nseg = (int)std::max<size_t>(1, (C + seg_cells - 1) / std::max(1, seg_cells));
+  std::unordered_map<uint32_t, size_t> at;
+  for (size_t k = 0; k < C; k++) at[mr.luts[k].root] = k;
+  auto nin_of = [](const Lut& L) { return L.kind == 1 ? 2 : (int)L.nin; };
+  // Rematerialisation: a cell whose whole cone (down to variables) has at
+  // most kRemat cells is recomputed in every segment that needs it instead of
+  // being stored -- the hash-consed DAG of a large term reuses many small
+  // subterms across the whole program.
+  const int kRemat = remat_cells;
+  std::vector<int> cone(C, 0);
+  for (size_t k = 0; k < C; k++) {
+    int c = 1;
+    const Lut& L = mr.luts[k];
+    for (int q = 0; q < nin_of(L) && c <= kRemat; q++) {
+      auto it = at.find(L.in[q]);
+      if (it != at.end()) c += cone[it->second];
+    }
+    cone[k] = std::min(c, kRemat + 1);  // inputs precede k in DFS post-order
+  }
+  auto remat = [&](uint32_t n) { auto it = at.find(n); return it != at.end() && cone[it->second] <= kRemat; };
+  auto seg_of = [&](size_t k) { return (int)(k / seg_cells); };
+  // last segment using each stored value (the output counts as used in the last)
+  std::unordered_map<uint32_t, int> last_use;
+  for (size_t k = 0; k < C; k++) {
+    const Lut& L = mr.luts[k];
+    for (int q = 0; q < nin_of(L); q++) {
+      auto it = at.find(L.in[q]);
+      if (it != at.end() && !remat(L.in[q]) && seg_of(it->second) < seg_of(k))
+        last_use[L.in[q]] = std::max(last_use[L.in[q]], seg_of(k));
+    }
+  }
+  const Lit out = b.outs[0];
+  {
+    auto it = at.find(lit_node(out));
+    if (it != at.end() && !remat(lit_node(out)) && seg_of(it->second) < nseg - 1) last_use[lit_node(out)] = nseg - 1;
+  }
+  // global slots, reused by liveness
+  std::unordered_map<uint32_t, uint32_t> slot;
+  std::vector<std::vector<uint32_t>> by_def(nseg);
+  for (auto& kv : last_use) by_def[seg_of(at[kv.first])].push_back(kv.first);
+  std::vector<std::pair<int, uint32_t>> busy;
+  std::vector<uint32_t> free_slots;
+  for (int sg = 0; sg < nseg; sg++) {
+    for (size_t i = 0; i < busy.size();)
+      if (busy[i].first <= sg) { free_slots.push_back(busy[i].second); busy[i] = busy.back(); busy.pop_back(); }
+      else i++;
+    std::sort(by_def[sg].begin(), by_def[sg].end());
+    for (uint32_t v : by_def[sg]) {
+      uint32_t sl;
+      if (!free_slots.empty()) { sl = free_slots.back(); free_slots.pop_back(); }
+      else sl = plan.n_slots++;
+      slot[v] = sl;
+      busy.push_back({last_use[v], sl});
+    }
+    plan.max_live = std::max<uint32_t>(plan.max_live, (uint32_t)busy.size());
+  }
+  std::unordered_map<uint32_t, std::vector<uint32_t>> var_nodes;
+  for (size_t q = 0; q < D.nodes.size(); q++)
+    if (D.nodes[q].kind == NK_VAR) var_nodes[D.nodes[q].val].push_back((uint32_t)q);
+  const bool want_count = mode == KM_COUNT || fuse_count;
+  for (int sg = 0; sg < nseg; sg++) {
+    std::ostringstream os;
+    os << "// generated by libbfa: segment " << sg << "/" << nseg << "\n" << kPrelude;
+    Emitter E(D, os);
+    for (const Lut& L : mr.luts) E.plan_cell(L);
+    const size_t k0 = (size_t)sg * seg_cells, k1 = std::min(C, k0 + seg_cells);
+    const bool last = sg == nseg - 1;
+    os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << thread_bits) << ")\n"
+       << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ gbuf, const u64 stride, "
+       << "u32* __restrict__ out, u64* __restrict__ count) {\n"
+       << "  u64 acc = 0;\n"
+       << "  const u64 gstride = (u64)gridDim.x * blockDim.x;\n"
+       << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += gstride) {\n"
+       << "    const u64 w = w_begin + k;\n";
+    // values available in this segment; everything is emitted at first use
+    std::unordered_map<uint32_t, uint8_t> avail;
+    std::function<void(uint32_t)> ensure = [&](uint32_t n) {
+      if (avail.count(n)) return;
+      const Node& nd = D.nodes[n];
+      if (nd.kind == NK_CONST) return;
+      avail[n] = 1;
+      if (nd.kind == NK_VAR) {
+        os << "    const u32 v" << nd.val << " = 0u - (u32)((w >> " << (b.pos[nd.val] - 5) << ") & 1ull);\n";
+        E.emit_derived(n, "    ");
+        return;
+      }
+      auto it = at.find(n);
+      if (it == at.end()) return;
+      const size_t k = it->second;
+      if ((size_t)k >= k0 && k < k1) { avail.erase(n); return; }  // defined later in this segment
+      if (remat(n)) {                                            // recompute the small cone here
+        const Lut& L = mr.luts[k];
+        for (int q = 0; q < nin_of(L); q++) ensure(L.in[q]);
+        E.lut(L, "    ");
+      } else {
+        os << "    const u32 " << E.name(n) << " = __ldcs(gbuf + " << slot.at(n) << "ull * stride + k);\n";
+        E.emit_derived(n, "    ");
+      }
+    };
+    for (size_t k = k0; k < k1; k++) {
+      const Lut& L = mr.luts[k];
+      for (int q = 0; q < nin_of(L); q++) ensure(L.in[q]);
+      E.lut(L, "    ");
+      avail[L.root] = 1;
+      auto it = slot.find(L.root);
+      if (it != slot.end()) os << "    __stcs(gbuf + " << it->second << "ull * stride + k, " << E.name(L.root) << ");\n";
+    }
+    if (last) {
+      ensure(lit_node(out));
+      os << "    const u32 r = (" << E.value(out) << ") & mask;\n";
+      if (mode == KM_EVAL) os << "    out[k] = r;\n";
+      if (want_count) os << "    acc += __popc(r);\n";
+    }
+    os << "  }\n";
+    if (last && want_count) os << "  bfa_block_sum(acc, count);\n";
+    os << "}\n";
+    plan.sources.push_back(os.str());
+    plan.cells.push_back((uint32_t)(k1 - k0));
+    plan.emitted += E.cells_emitted;
+  }
+  return plan;
 }
 
 InterpProgram build_interp(const Parsed& prog) {

@@ -166,6 +166,23 @@ struct InterpProgram {
 };
 InterpProgram build_interp(const Parsed& prog);
 
+// Segmented execution for programs too large for one straight-line kernel
+// (the paper's 2^17-node term): the generic cover in
+// depth-first order is cut into segments of <= seg_cells cells; segment i is
+// kernel i.  Values used after their segment live in global slot arrays
+// (slot-major, `stride` words per slot).  Kernel signature:
+//   (u64 w_begin, u64 w_count, u32 mask, u32* gbuf, u64 stride, u32* out, u64* count)
+// and only the last segment counts / stores the result.
+struct SegPlan {
+  std::vector<std::string> sources;
+  std::vector<uint32_t> cells;     // per segment
+  uint32_t n_slots = 0;
+  uint32_t max_live = 0;           // most values crossing one boundary
+  uint64_t emitted = 0;            // cells emitted incl. rematerialised ones
+};
+SegPlan emit_segmented(const Parsed& prog, KernelMode mode, bool fuse_count, int seg_cells, int thread_bits,
+                       int imad_cost_pct = 50, int remat = 6);
+
 // LUT cover IR text (bfa_dump what=0) and the plain cover size L.
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts);
 

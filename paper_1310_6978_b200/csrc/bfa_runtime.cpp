@@ -153,6 +153,8 @@ struct Options {
   int min_blocks = 0;
   int role_search = 1;
   int role_budget = 200;
+  int segment_cells = 0;   // 0: auto (segment when L > 8000), > 0: always, this many cells
+  int segment_remat = 2;   // recompute shared cells with cones <= this many cells
 };
 
 struct JitEntry {
@@ -174,6 +176,7 @@ struct bfa_prog {
   std::map<std::string, std::unique_ptr<JitEntry>> jit;
   std::unique_ptr<bfa::InterpProgram> interp;  // engine=1 ablation
   std::map<std::string, std::vector<int8_t>> roles;  // role-search results
+  std::map<std::string, std::unique_ptr<bfa::SegPlan>> segplans;
 };
 
 namespace {
@@ -249,6 +252,48 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
       if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
       int nb = 1;
       drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 1 << spec.thread_bits, 0);
+      drv().FuncGetAttribute(&e->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
+      e->occupancy[dev] = std::max(1, nb);
+      f = e->fn.emplace(dev, k).first;
+    }
+    if (fn) *fn = f->second;
+  }
+  if (out) *out = e;
+  return BFA_OK;
+}
+
+// As get_kernel, for a kernel whose source is already generated (segments).
+int get_kernel_src(const bfa_prog* cp, const std::string& key, const std::string& src, int thread_bits, int dev,
+                   JitEntry** out, CUfunction* fn) {
+  bfa_prog* p = const_cast<bfa_prog*>(cp);
+  JitEntry* e = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->jit.find(key);
+    if (it != p->jit.end()) e = it->second.get();
+  }
+  if (!e) {
+    auto ne = std::make_unique<JitEntry>();
+    ne->source = src;
+    int rc = nvrtc_compile(ne->source, &ne->cubin);
+    if (rc) return rc;
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto it = p->jit.find(key);
+    if (it == p->jit.end()) it = p->jit.emplace(key, std::move(ne)).first;
+    e = it->second.get();
+  }
+  if (dev >= 0) {
+    std::lock_guard<std::mutex> lk(p->mu);
+    auto f = e->fn.find(dev);
+    if (f == e->fn.end()) {
+      CUmodule mod;
+      CUresult r = drv().ModuleLoadData(&mod, e->cubin.data());
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleLoadData: %s", cu_str(r).c_str());
+      CUfunction k;
+      r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      int nb = 1;
+      drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 1 << thread_bits, 0);
       drv().FuncGetAttribute(&e->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
       e->occupancy[dev] = std::max(1, nb);
       f = e->fn.emplace(dev, k).first;
@@ -359,6 +404,87 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     return BFA_OK;
   }
   const int T = 1 << o.thread_bits;
+  const int seg = o.segment_cells ? o.segment_cells : (p->info.luts > 8000 ? 768 : 0);
+  if (seg > 0 && !enumerate) {
+    // NEXT-3: program too large for one straight-line kernel -> segments
+    bfa_prog* mp = const_cast<bfa_prog*>(p);
+    const bfa::KernelMode mode = eval ? bfa::KM_EVAL : bfa::KM_COUNT;
+    const bool fuse = eval && count_dev != nullptr;
+    const std::string pkey = "seg" + std::to_string((int)mode) + (fuse ? "f" : "-") + std::to_string(seg) + "." +
+                             std::to_string(o.thread_bits) + "i" + std::to_string(o.dual_pipe ? o.imad_cost_pct : 0) +
+                             "r" + std::to_string(o.segment_remat);
+    bfa::SegPlan* plan = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(mp->mu);
+      auto it = mp->segplans.find(pkey);
+      if (it != mp->segplans.end()) plan = it->second.get();
+    }
+    if (!plan) {
+      auto np = std::make_unique<bfa::SegPlan>(bfa::emit_segmented(
+          p->parsed, mode, fuse, seg, o.thread_bits, o.dual_pipe ? o.imad_cost_pct : 0, o.segment_remat));
+      std::lock_guard<std::mutex> lk(mp->mu);
+      auto it = mp->segplans.find(pkey);
+      if (it == mp->segplans.end()) it = mp->segplans.emplace(pkey, std::move(np)).first;
+      plan = it->second.get();
+    }
+    const size_t nseg = plan->sources.size();
+    std::vector<CUfunction> fns(nseg);
+    std::vector<JitEntry*> jes(nseg, nullptr);
+    {  // compile all segments in parallel
+      std::vector<int> rcs(nseg, 0);
+      std::vector<std::thread> th;
+      const size_t par = std::max<size_t>(1, std::thread::hardware_concurrency());
+      for (size_t b0 = 0; b0 < nseg; b0 += par) {
+        th.clear();
+        for (size_t i = b0; i < std::min(nseg, b0 + par); i++)
+          th.emplace_back([&, i] {
+            rcs[i] = get_kernel_src(p, pkey + "#" + std::to_string(i), plan->sources[i], o.thread_bits, -1, &jes[i],
+                                    nullptr);
+          });
+        for (auto& t : th) t.join();
+      }
+      for (size_t i = 0; i < nseg; i++) {
+        if (rcs[i]) return rcs[i];
+        rc = get_kernel_src(p, pkey + "#" + std::to_string(i), plan->sources[i], o.thread_bits, dev, &jes[i], &fns[i]);
+        if (rc) return rc;
+      }
+    }
+    // slot arrays in HBM, processed in tiles of words (<= 16 GiB of slots)
+    const uint64_t W = whi - wlo;
+    const uint64_t slots = std::max<uint32_t>(1, plan->n_slots);
+    uint64_t tile = std::min<uint64_t>(W, (16ull << 30) / (slots * 4));
+    tile = std::max<uint64_t>(tile, 1);
+    uint32_t* gbuf = nullptr;
+    cudaError_t e2 = cudaMallocAsync(&gbuf, slots * tile * 4, st);
+    if (e2 != cudaSuccess) return set_err(BFA_E_NOMEM, "segment slots (%llu x %llu words): %s",
+                                          (unsigned long long)slots, (unsigned long long)tile, cudaGetErrorString(e2));
+    uint32_t* out32s = reinterpret_cast<uint32_t*>(out_dev);
+    int kernels = 0;
+    for (uint64_t t0 = 0; t0 < W && rc == BFA_OK; t0 += tile) {
+      uint64_t wb = wlo + t0, wc = std::min(tile, W - t0), stride = tile;
+      uint32_t* o32 = eval ? out32s + t0 : nullptr;
+      uint64_t* cnt = count_dev;
+      for (size_t i = 0; i < nseg && rc == BFA_OK; i++) {
+        const int bps = jes[i]->occupancy[dev];
+        unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((wc + T - 1) / T, (uint64_t)di.sms * bps));
+        void* args[] = {&wb, &wc, &mask, &gbuf, &stride, &o32, &cnt};
+        rc = launch(fns[i], grid, T, st, args);
+        kernels++;
+      }
+    }
+    cudaFreeAsync(gbuf, st);
+    if (rc) return rc;
+    int maxregs = 0;
+    for (auto* je : jes) maxregs = std::max(maxregs, je->regs);
+    std::ostringstream js;
+    js << "{\"device\": " << dev << ", \"variant\": \"segmented\", \"segments\": " << nseg
+       << ", \"cells\": " << [&] { uint64_t c = 0; for (auto x : plan->cells) c += x; return c; }()
+       << ", \"emitted\": " << plan->emitted << ", \"slots\": " << plan->n_slots << ", \"max_live\": " << plan->max_live
+       << ", \"tile_words\": " << tile
+       << ", \"max_regs\": " << maxregs << ", \"kernels\": " << kernels << "}";
+    g_last_launch = js.str();
+    return BFA_OK;
+  }
   // full-chip grid estimate for planning (exact occupancy comes from the kernel)
   const int full_grid = di.sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
   // eval stores 2^s consecutive words per thread as one vector store: the
@@ -585,6 +711,8 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
   else if (k == "role_search") { if (v < 0 || v > 1) return bad(); p->opt.role_search = (int)v; }
   else if (k == "role_budget") { if (v < 1 || v > 4096) return bad(); p->opt.role_budget = (int)v; }
+  else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }
+  else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -635,8 +763,8 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   std::ostringstream js;
-  if (n < 24 || p->opt.force_generic || p->opt.engine) {
-    js << "{\"skipped\": \"problem too small or generic/interpreter engine\"}";
+  if (n < 24 || p->opt.force_generic || p->opt.engine || p->opt.segment_cells || p->info.luts > 8000) {
+    js << "{\"skipped\": \"problem too small, generic/interpreter engine, or segmented program\"}";
     if (report && len) snprintf(report, len, "%s", js.str().c_str());
     return BFA_OK;
   }
@@ -978,6 +1106,22 @@ int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
   std::string s;
   if (what == 0) {
     s = bfa::dump_ir(p->parsed, nullptr);
+  } else if (what == 5 || what == 6) {
+    // 5: segmented-execution plan summary (JSON); 6: source of segment n
+    const int seg = p->opt.segment_cells ? p->opt.segment_cells : 768;
+    bfa::SegPlan plan = bfa::emit_segmented(p->parsed, bfa::KM_COUNT, false, seg, p->opt.thread_bits,
+                                            p->opt.dual_pipe ? p->opt.imad_cost_pct : 0, p->opt.segment_remat);
+    if (what == 6) {
+      if (n < 0 || n >= (int)plan.sources.size()) return set_err(BFA_E_ARG, "segment %d of %zu", n, plan.sources.size());
+      s = plan.sources[n];
+    } else {
+      std::ostringstream js;
+      js << "{\"segments\": " << plan.sources.size() << ", \"slots\": " << plan.n_slots << ", \"max_live\": "
+         << plan.max_live << ", \"emitted\": " << plan.emitted << ", \"cells\": [";
+      for (size_t i = 0; i < plan.cells.size(); i++) js << (i ? ", " : "") << plan.cells[i];
+      js << "]}";
+      s = js.str();
+    }
   } else {
     bfa::KernelSpec spec;
     int rc = spec_for_what_n(p, what, n, &spec);

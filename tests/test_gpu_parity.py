@@ -84,7 +84,7 @@ GEOMETRIES = [dict(slot_bits=0, thread_bits=5, inner_bits=0), dict(slot_bits=1, 
               dict(slot_bits=3, thread_bits=7, inner_bits=3), dict(slot_bits=2, thread_bits=8, inner_bits=4),
               dict(force_generic=1), dict(imad_cost_pct=20), dict(imad_cost_pct=20, force_generic=1),
               dict(dual_pipe=0), dict(slot_bits=5, imad_cost_pct=50), dict(slot_bits=4, inner_bits=2, min_blocks=2),
-              dict(engine=1)]
+              dict(engine=1), dict(segment_cells=40), dict(segment_cells=16, segment_remat=0)]
 
 
 @pytest.mark.parametrize("geo", range(len(GEOMETRIES)))
@@ -257,6 +257,25 @@ def test_autotune_keeps_results():
     lo = (1 << 36) - (1 << 22)
     ow, oc = oracle.evaluate(text, n, lo, 1 << 36)
     assert np.array_equal(host(p.eval_range(n, lo, 1 << 36)), ow)
+
+
+# ------------------------------------------------------------ NEXT-3
+def test_paper_scale_term_segmented():
+    """SURVEY §8(f) NEXT-3, the paper's timed experiment shape (PAPER.md:
+    374-380): a 30-variable term with 2^17 tree nodes runs as segmented
+    kernels.  Oracle sub-cube counts and vectors agree; count(f) + count(~f)
+    = 2^30 over the full cube."""
+    text, n, _ = W.config("paper_2p17")
+    p = bfa.Program(text)
+    c = p.count(n)
+    ll = bfa.last_launch()
+    assert ll["variant"] == "segmented" and ll["segments"] > 8
+    body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+    assert c + bfa.Program(f"{body}\n~{out}").count(n) == 1 << n
+    lo = 3 << 24
+    ow, oc = oracle.evaluate(text, n, lo, lo + (1 << 14))
+    assert int(p.count_range(n, lo, lo + (1 << 14)).item()) == oc
+    assert np.array_equal(host(p.eval_range(n, lo, lo + (1 << 14))), ow)
 
 
 # ------------------------------------------------------------ NEXT-1 / NEXT-2

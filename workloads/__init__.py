@@ -178,6 +178,54 @@ def random_dag(n: int, gates: int, seed: int = SEED, window: int = 32) -> str:
 
 
 # --------------------------------------------------------------------------
+# paper-scale term (NEXT-3): 30 variables, 2^17 expression-tree nodes
+# --------------------------------------------------------------------------
+def paper_scale_tree(n: int = 30, nodes: int = 1 << 17, seed: int = SEED) -> str:
+    """A random binary expression TREE with `nodes` nodes (2^16 literal leaves
+    and 2^16 - 1 binary operators for the default), the shape of the paper's
+    timed experiment "a Boolean term t with 30 variables and 2^17 nodes"
+    (PAPER.md:374-380).  Leaves are variables (uniform, negated p=1/2);
+    operators are paired level by level (a balanced tree of depth 16) with op
+    AND/OR/XOR/IFF uniform so the term neither collapses to a constant nor
+    loses its dependence on the leaves.  Emitted as one `let` per level-16
+    subtree of 64 leaves so the text stays parseable by line."""
+    rng = np.random.default_rng(seed)
+    leaves = (nodes + 1) // 2
+    ops = ("&", "|", "^", "<->")
+    level = []
+    for _ in range(leaves):
+        v = int(rng.integers(0, n))
+        level.append(("~" if rng.random() < 0.5 else "") + f"x{v}")
+    lines = []
+    group = 64
+    names = []
+    for g in range(0, leaves, group):
+        cur = level[g:g + group]
+        while len(cur) > 1:
+            nxt = []
+            for i in range(0, len(cur) - 1, 2):
+                nxt.append(f"({cur[i]} {ops[int(rng.integers(0, 4))]} {cur[i + 1]})")
+            if len(cur) & 1:
+                nxt.append(cur[-1])
+            cur = nxt
+        name = f"t{len(names)}"
+        lines.append(f"let {name} = {cur[0]}")
+        names.append(name)
+    cur = names
+    while len(cur) > 1:
+        nxt = []
+        for i in range(0, len(cur) - 1, 2):
+            name = f"u{len(lines)}"
+            lines.append(f"let {name} = {cur[i]} {ops[int(rng.integers(0, 4))]} {cur[i + 1]}")
+            nxt.append(name)
+        if len(cur) & 1:
+            nxt.append(cur[-1])
+        cur = nxt
+    lines.append(cur[0])
+    return _program(lines)
+
+
+# --------------------------------------------------------------------------
 # random terms for the parity suite (SURVEY.md §8(d), SPEC acceptance 1)
 # --------------------------------------------------------------------------
 # term = ('var', i) | ('const', b) | ('not', t) | (op, a, b), op in
@@ -307,4 +355,6 @@ def config(name: str):
         return posets(6), 36, 130023
     if name == "c5":
         return random_dag(42, 1000, C5_SEED), 42, None
+    if name == "paper_2p17":
+        return paper_scale_tree(30, 1 << 17), 30, None
     raise KeyError(name)
