@@ -180,6 +180,17 @@ int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_pro
 int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* mu_out, uint64_t capacity,
                   uint64_t* count_dev, void* stream);
 
+/* Batched counting (the counting procedure TBA runs
+ * one reduced program per c-partition): many programs in
+ * ONE launch.  bfa_batch_create JIT-compiles a kernel holding every program
+ * (the programs must outlive the batch); bfa_batch_count counts program i
+ * over all 2^ns[i] valuations into counts_dev[i] (device, `count` u64),
+ * synchronous on `stream`.  Meant for many small programs. */
+typedef struct bfa_batch bfa_batch;
+int bfa_batch_create(const bfa_prog* const* progs, int count, bfa_batch** out);
+int bfa_batch_count(bfa_batch* b, const int* ns, uint64_t* counts_dev, void* stream);
+void bfa_batch_free(bfa_batch* b);                          /* NULL-safe */
+
 /* ---- materialised mode (the paper's vector formulation) ---- */
 
 /* Fill the generator table S: row v (0 <= v < n_rows) is

@@ -13,7 +13,7 @@ import ctypes
 import json
 import os
 
-__all__ = ["Program", "BfaError", "words_for", "reinstate", "last_launch", "fill_generators", "popcount",
+__all__ = ["Program", "Batch", "BfaError", "words_for", "reinstate", "last_launch", "fill_generators", "popcount",
            "peak_int", "lib_path", "version"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -47,6 +47,9 @@ _SIGS = {
                               _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
     "bfa_enumerate": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_uint64,
                                  _c.c_void_p, _c.c_void_p]),
+    "bfa_batch_create": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(_c.c_void_p)]),
+    "bfa_batch_count": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int), _c.c_void_p, _c.c_void_p]),
+    "bfa_batch_free": (None, [_c.c_void_p]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -236,6 +239,28 @@ class Program:
         buf = ctypes.create_string_buffer(size)
         _check(lib.bfa_jit_cubin(self._h, what, n, buf, size))
         return buf.raw
+
+
+class Batch:
+    """bfa_batch_*: count many programs in one launch (NEXT-4)."""
+
+    def __init__(self, programs):
+        self.programs = list(programs)              # keep them alive
+        arr = (ctypes.c_void_p * len(self.programs))(*[p._h.value for p in self.programs])
+        h = ctypes.c_void_p()
+        _check(_load().bfa_batch_create(arr, len(self.programs), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.bfa_batch_free(self._h)
+            self._h = None
+
+    def count(self, ns, out=None, stream=None):
+        out = _u64_out(out, len(self.programs))
+        arr = (ctypes.c_int * len(self.programs))(*ns)
+        _check(_load().bfa_batch_count(self._h, arr, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+        return out
 
 
 def reinstate(mu_free, free_ids, assignment: dict) -> list:

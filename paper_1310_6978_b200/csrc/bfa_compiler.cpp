@@ -1211,6 +1211,56 @@ SegPlan emit_segmented(const Parsed& prog, KernelMode mode, bool fuse_count, int
   return plan;
 }
 
+std::string emit_batch(const std::vector<const Parsed*>& progs, int thread_bits) {
+  std::ostringstream os;
+  os << "// generated by libbfa: batch of " << progs.size() << " programs\n" << kPrelude;
+  KernelSpec spec;
+  spec.mode = KM_COUNT;
+  spec.generic = true;
+  spec.slot_bits = 0;
+  spec.thread_bits = thread_bits;
+  spec.inner_bits = 0;
+  spec.dual_pipe = 0;
+  for (size_t j = 0; j < progs.size(); j++) {
+    Built b;
+    build_specialised(*progs[j], spec, &b);
+    MapResult mr = choose_mapping(b, spec, nullptr, nullptr);
+    dfs_order(&mr, b.outs);
+    Emitter E(b.D, os);
+    os << "__device__ __noinline__ u32 bfa_prog_" << j << "(const u64 w) {\n";
+    std::vector<uint8_t> used(64, 0);
+    for (const Lut& L : mr.luts)
+      for (int q = 0; q < L.nin; q++)
+        if (b.D.nodes[L.in[q]].kind == NK_VAR) used[b.D.nodes[L.in[q]].val] = 1;
+    if (b.D.nodes[lit_node(b.outs[0])].kind == NK_VAR) used[b.D.nodes[lit_node(b.outs[0])].val] = 1;
+    for (int v = 0; v < 64; v++)
+      if (used[v]) os << "  const u32 v" << v << " = 0u - (u32)((w >> " << (b.pos[v] - 5) << ") & 1ull);\n";
+    for (const Lut& L : mr.luts) E.lut(L, "  ");
+    os << "  return " << E.value(b.outs[0]) << ";\n}\n";
+  }
+  os << "extern \"C\" __global__ void __launch_bounds__(" << (1 << thread_bits) << ")\n"
+     << "bfa_kernel(const u64* __restrict__ start, const u32* __restrict__ masks, const u64* __restrict__ words, "
+     << "const int nprog, const u64 total, u64* __restrict__ counts) {\n"
+     << "  const u64 gstride = (u64)gridDim.x * blockDim.x;\n"
+     << "  for (u64 g = (u64)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gstride) {\n"
+     << "    // program of this word: warp-uniform (ranges are padded to whole warps)\n"
+     << "    int lo = 0, hi = nprog - 1;\n"
+     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (start[mid] <= g) lo = mid; else hi = mid - 1; }\n"
+     << "    const u64 k = g - start[lo];\n"
+     << "    u32 r = 0;\n"
+     << "    if (k < words[lo]) {\n"
+     << "      switch (lo) {\n";
+  for (size_t j = 0; j < progs.size(); j++) os << "        case " << j << ": r = bfa_prog_" << j << "(k); break;\n";
+  os << "      }\n"
+     << "      r &= masks[lo];\n"
+     << "    }\n"
+     << "    u32 c = __reduce_add_sync(0xffffffffu, (u32)__popc(r));\n"
+     << "    if ((threadIdx.x & 31u) == 0 && c) atomicAdd(counts + lo, (u64)c);\n"
+     << "  }\n"
+     << "}\n";
+  return os.str();
+}
+
 InterpProgram build_interp(const Parsed& prog) {
   // the generic specialisation: lanes 0-4 as word constants, variables >= 5
   // computed from the word index; plain LUT3 cover

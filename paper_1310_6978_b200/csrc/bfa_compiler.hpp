@@ -183,6 +183,14 @@ struct SegPlan {
 SegPlan emit_segmented(const Parsed& prog, KernelMode mode, bool fuse_count, int seg_cells, int thread_bits,
                        int imad_cost_pct = 50, int remat = 6);
 
+// Batched counting: one kernel for many programs.
+// Program j is a __noinline__ device function of its word index; the kernel
+// walks a global word space in which program j owns [start[j], start[j+1])
+// (each padded to whole warps) and accumulates counts[j].  Kernel signature:
+//   (const u64* start, const u32* masks, const u64* words, int nprog,
+//    u64 total, u64* counts)
+std::string emit_batch(const std::vector<const Parsed*>& progs, int thread_bits);
+
 // LUT cover IR text (bfa_dump what=0) and the plain cover size L.
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts);
 

@@ -592,6 +592,18 @@ int spec_for_what_n(const bfa_prog* p, int what, int n, bfa::KernelSpec* spec) {
 
 }  // namespace
 
+// batched counting (NEXT-4)
+struct bfa_batch_s {
+  std::vector<const bfa_prog*> progs;
+  std::vector<int> max_var;
+  std::string source;
+  std::vector<char> cubin;
+  std::map<int, CUfunction> fn;
+  std::map<int, int> occupancy;
+  int regs = 0;
+  std::mutex mu;
+};
+
 // ================================================================ C ABI
 #pragma GCC visibility push(default)
 extern "C" {
@@ -872,6 +884,97 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
      << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
      << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits << "}}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
+  return BFA_OK;
+}
+
+int bfa_batch_create(const bfa_prog* const* progs, int count, bfa_batch** out) {
+  if (!progs || !out || count <= 0) return set_err(BFA_E_ARG, "bad batch");
+  auto b = std::make_unique<bfa_batch_s>();
+  std::vector<const bfa::Parsed*> ps;
+  for (int i = 0; i < count; i++) {
+    if (!progs[i]) return set_err(BFA_E_ARG, "NULL program %d in batch", i);
+    b->progs.push_back(progs[i]);
+    b->max_var.push_back(progs[i]->info.max_var_id);
+    ps.push_back(&progs[i]->parsed);
+  }
+  b->source = bfa::emit_batch(ps, 8);
+  int rc = nvrtc_compile(b->source, &b->cubin);
+  if (rc) return rc;
+  *out = reinterpret_cast<bfa_batch*>(b.release());
+  return BFA_OK;
+}
+
+void bfa_batch_free(bfa_batch* b) { delete reinterpret_cast<bfa_batch_s*>(b); }
+
+int bfa_batch_count(bfa_batch* bh, const int* ns, uint64_t* counts_dev, void* stream) {
+  bfa_batch_s* b = reinterpret_cast<bfa_batch_s*>(bh);
+  if (!b || !ns || !counts_dev) return set_err(BFA_E_ARG, "NULL argument");
+  const int np = (int)b->progs.size();
+  std::vector<uint64_t> start(np + 1, 0), words(np);
+  std::vector<uint32_t> masks(np);
+  for (int i = 0; i < np; i++) {
+    const int n = ns[i];
+    if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "program %d: n=%d outside [0, 63]", i, n);
+    if (b->max_var[i] >= n) return set_err(BFA_E_RANGE, "program %d uses x%d >= n=%d", i, b->max_var[i], n);
+    words[i] = n < 5 ? 1 : (1ull << (n - 5));
+    masks[i] = n < 5 ? (uint32_t)((1ull << (1u << n)) - 1ull) : 0xFFFFFFFFu;
+    start[i + 1] = start[i] + ((words[i] + 31) & ~31ull);
+  }
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  CUfunction fn;
+  int occ;
+  {
+    std::lock_guard<std::mutex> lk(b->mu);
+    auto f = b->fn.find(dev);
+    if (f == b->fn.end()) {
+      CUmodule mod;
+      CUresult r = drv().ModuleLoadData(&mod, b->cubin.data());
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleLoadData: %s", cu_str(r).c_str());
+      CUfunction k;
+      r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
+      if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      int nb = 1;
+      drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0);
+      drv().FuncGetAttribute(&b->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
+      b->occupancy[dev] = std::max(1, nb);
+      f = b->fn.emplace(dev, k).first;
+    }
+    fn = f->second;
+    occ = b->occupancy[dev];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  // the three tables in one device allocation
+  const size_t bytes = (np + 1) * 8 + np * 8 + np * 4;
+  std::vector<char> host(bytes);
+  memcpy(host.data(), start.data(), (np + 1) * 8);
+  memcpy(host.data() + (np + 1) * 8, words.data(), np * 8);
+  memcpy(host.data() + (np + 1) * 8 + np * 8, masks.data(), np * 4);
+  char* dtab = nullptr;
+  cudaError_t e = cudaMallocAsync(&dtab, bytes, st);
+  if (e != cudaSuccess) return set_err(BFA_E_NOMEM, "batch tables: %s", cudaGetErrorString(e));
+  e = cudaMemcpyAsync(dtab, host.data(), bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(counts_dev, 0, np * 8, st);
+  if (e != cudaSuccess) { cudaFreeAsync(dtab, st); return set_err(BFA_E_CUDA, "batch: %s", cudaGetErrorString(e)); }
+  const uint64_t* d_start = reinterpret_cast<const uint64_t*>(dtab);
+  const uint64_t* d_words = reinterpret_cast<const uint64_t*>(dtab + (np + 1) * 8);
+  const uint32_t* d_masks = reinterpret_cast<const uint32_t*>(dtab + (np + 1) * 8 + np * 8);
+  uint64_t total = start[np];
+  int nprog = np;
+  unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)di.sms * occ));
+  void* args[] = {&d_start, &d_masks, &d_words, &nprog, &total, &counts_dev};
+  rc = launch(fn, grid, 256, st, args);
+  // the host staging buffer must outlive the async copy
+  cudaError_t se = cudaStreamSynchronize(st);
+  cudaFreeAsync(dtab, st);
+  if (rc) return rc;
+  if (se != cudaSuccess) return set_err(BFA_E_CUDA, "batch: %s", cudaGetErrorString(se));
+  std::ostringstream js;
+  js << "{\"device\": " << dev << ", \"variant\": \"batch\", \"programs\": " << np << ", \"words\": " << total
+     << ", \"grid\": " << grid << ", \"regs\": " << b->regs << ", \"kernels\": 1}";
+  g_last_launch = js.str();
   return BFA_OK;
 }
 

@@ -259,6 +259,41 @@ def test_autotune_keeps_results():
     assert np.array_equal(host(p.eval_range(n, lo, 1 << 36)), ow)
 
 
+# ------------------------------------------------------------ NEXT-4
+def test_batch_counts(golden):
+    """Batched counting: many programs in one launch give the same counts as
+    the closed forms, the oracle, and one launch per program."""
+    progs, ns, expect = [], [], []
+    cf = golden("closed_forms.json")
+    for fam in ("posets", "equivalences", "linear_orders"):
+        for k, c in zip(cf[fam]["k"], cf[fam]["count"]):
+            if k <= 5:
+                progs.append(bfa.Program(getattr(W, fam)(k))); ns.append(k * k); expect.append(c)
+    for seed in range(60):
+        rp = W.random_program(seed, max_n=20)
+        progs.append(bfa.Program(rp.text)); ns.append(rp.n); expect.append(oracle.count(rp.text, rp.n))
+    b = bfa.Batch(progs)
+    got = b.count(ns).cpu().tolist()
+    assert got == expect
+    assert bfa.last_launch()["kernels"] == 1
+
+
+def test_batch_cofactors_of_c4():
+    """The 64 cofactors of C4 over its top 6 letters (bfa_assume), counted
+    as one batch, sum to 130023 and each equals the count of its sub-cube."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text)
+    cof = []
+    for r in range(64):
+        a = {30 + b: (r >> b) & 1 for b in range(6)}
+        q, nf, _ = p.assume(n, a)
+        cof.append(q)
+    got = bfa.Batch(cof).count([30] * 64).cpu().tolist()
+    assert sum(got) == expect
+    for r in (0, 37, 63):
+        assert got[r] == int(p.count_range(n, r << 30, (r + 1) << 30).item())
+
+
 # ------------------------------------------------------------ NEXT-3
 def test_paper_scale_term_segmented():
     """SURVEY §8(f) NEXT-3, the paper's timed experiment shape (PAPER.md:
