@@ -228,7 +228,9 @@ def run_bfa(args):
 
     # autotune (JIT of the candidate variants + probe timing; untimed), then
     # warm-up.  Rank 0 tunes and broadcasts its choice so every rank runs the
-    # same kernel.
+    # same kernel.  The one-time preparation cost (tuning, role search,
+    # cofactor split, NVRTC) is reported as jit_prep_s.
+    t_prep = time.perf_counter()
     tune = prog.autotune(n, k_free=n - (world.bit_length() - 1)) if rank == 0 else None
     if world > 1:
         obj = [tune]
@@ -236,8 +238,11 @@ def run_bfa(args):
         tune = obj[0]
     for key, val in ((tune or {}).get("best") or {}).items():
         prog.set_option(key, val)
-    for _ in range(max(args.warmup, 3)):
+    for i in range(max(args.warmup, 3)):
         step()
+        if i == 0:
+            torch.cuda.synchronize()
+            t_prep = time.perf_counter() - t_prep
     torch.cuda.synchronize()
     launch = bfa.last_launch()
     result = int(cnt.item()) & ((1 << 64) - 1)
@@ -289,8 +294,10 @@ def run_bfa(args):
     # loop-invariant cells hoisted: LOP3 cells on the ALU pipe,
     # IMAD cells (+ their operand registers) on the FMA pipe.
     if launch.get("variant") == "segmented":      # NEXT-3: every cell per word, LOP3 only
-        lop3_w, imad_w = launch["cells"] / 1.0, 0.0
-        lop3_w = launch.get("emitted", launch["cells"])
+        lop3_w, imad_w = launch.get("emitted", launch["cells"]), 0.0
+    elif "cells_lop3" in launch:                   # executed cells summed over all launches
+        lop3_w = launch["cells_lop3"] / words_per_launch
+        imad_w = launch["cells_imad"] / words_per_launch
     else:
         seg = max(launch["segments"], key=lambda g: g["words"])
         S, m = seg["words_per_iter"], seg["m"]
@@ -354,6 +361,15 @@ def run_bfa(args):
         "kernel_ms_per_step": kernel_s * 1e3,
         "launch": launch,
         "autotune": tune,
+        "jit_prep_s": t_prep,
+        "executed_valuations_per_s": (
+            ((1 << n) - launch["constant_zero"] * launch["valuations_per_cofactor"]) * args.steps / t_total
+            if launch.get("variant") == "kernel-cofactored" else value),
+        "decided_at_compile_time": (
+            {"valuations": launch["constant_zero"] * launch["valuations_per_cofactor"],
+             "how": "kernel-level cofactors the Reduction proved identically 0 (no models, no launch); "
+                    "prepared once in warm-up, reused every step"} if launch.get("variant") == "kernel-cofactored"
+            else None),
         "clocks": clk,
     }
     print(json.dumps(line), flush=True)

@@ -401,6 +401,45 @@ Parsed assume(const Parsed& src, int n, uint64_t mask, uint64_t values, std::vec
   return out;
 }
 
+uint32_t gate_count(const Parsed& p) {
+  std::vector<uint8_t> seen(p.dag.nodes.size(), 0);
+  std::vector<uint32_t> st{lit_node(p.root)};
+  uint32_t g = 0;
+  while (!st.empty()) {
+    uint32_t k = st.back(); st.pop_back();
+    if (seen[k]) continue;
+    seen[k] = 1;
+    const Node& nd = p.dag.nodes[k];
+    if (nd.kind == NK_GATE) { g++; st.push_back(nd.a); st.push_back(nd.b); }
+  }
+  return g;
+}
+
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j) {
+  std::vector<int> chosen;
+  for (int step = 0; step < j; step++) {
+    int best_v = -1;
+    uint64_t best = UINT64_MAX;
+    for (int v = 0; v < k; v++) {
+      if (!((p.support_mask >> v) & 1) || std::find(chosen.begin(), chosen.end(), v) != chosen.end()) continue;
+      uint64_t mask = 1ull << v;
+      for (int c : chosen) mask |= 1ull << c;
+      uint64_t total = 0;
+      for (uint64_t a = 0; a < (1ull << (chosen.size() + 1)) && total < best; a++) {
+        uint64_t values = 0;
+        int bit = 0;
+        for (int c : chosen) values |= ((a >> bit++) & 1) << c;
+        values |= ((a >> bit) & 1) << v;
+        total += gate_count(assume(p, k, mask, values, nullptr));
+      }
+      if (total < best) { best = total; best_v = v; }
+    }
+    if (best_v < 0) break;
+    chosen.push_back(best_v);
+  }
+  return chosen;
+}
+
 // ============================================================== LUT3 mapping
 namespace {
 

@@ -85,6 +85,13 @@ int parse_program(const std::string& text, Parsed* out, std::string* err);
 // old id.
 Parsed assume(const Parsed& src, int n, uint64_t mask, uint64_t values, std::vector<int>* free_ids);
 
+// Number of gates reachable from the root.
+uint32_t gate_count(const Parsed& p);
+
+// Kernel-level cofactoring: greedily pick j of the variables < k whose
+// 2^j cofactors (bfa_assume) have the fewest gates in total after Reduction.
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j);
+
 // ---------------------------------------------------------------- mapping
 struct Lut {
   uint32_t root;      // node id in the mapped DAG

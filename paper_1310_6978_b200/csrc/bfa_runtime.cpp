@@ -17,6 +17,7 @@
 #include <nvrtc.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -36,6 +37,9 @@ namespace {
 
 thread_local std::string g_err;
 thread_local std::string g_last_launch = "{}";
+// executed integer cells (LOP3 + IMAD + IMAD operand registers) of the last
+// launch sequence, split by pipe; the bench's roofline numerator
+thread_local double g_cells_lop3 = 0, g_cells_imad = 0;
 
 int set_err(int code, const char* fmt, ...) {
   char buf[2048];
@@ -155,6 +159,7 @@ struct Options {
   int role_budget = 200;
   int segment_cells = 0;   // 0: auto (segment when L > 8000), > 0: always, this many cells
   int segment_remat = 2;   // recompute shared cells with cones <= this many cells
+  int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
 };
 
 struct JitEntry {
@@ -177,6 +182,7 @@ struct bfa_prog {
   std::unique_ptr<bfa::InterpProgram> interp;  // engine=1 ablation
   std::map<std::string, std::vector<int8_t>> roles;  // role-search results
   std::map<std::string, std::unique_ptr<bfa::SegPlan>> segplans;
+  std::map<std::string, std::vector<std::unique_ptr<bfa_prog>>> cofactors;  // kernel-level cofactoring
 };
 
 namespace {
@@ -340,8 +346,8 @@ std::vector<Segment> plan(const Options& o, int s, int n, uint64_t wlo, uint64_t
 }
 
 // Common body of count_range / eval_range.
-int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
+int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
+                   cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out, uint64_t cap, bool accumulate) {
   const bool enumerate = mu_out != nullptr;
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
@@ -364,7 +370,8 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   if (rc) return rc;
 
   cudaError_t ce;
-  if (count_dev) {
+  if (!accumulate) g_cells_lop3 = g_cells_imad = 0;
+  if (count_dev && !accumulate) {
     ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
     if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
   }
@@ -537,6 +544,13 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     }
     if (rc) return rc;
     kernels++;
+    {
+      const double S = je->stats.words_per_iter, it = std::pow(2.0, spec.inner_bits);
+      const double words = (double)(sg.we - sg.wb);
+      g_cells_lop3 += words * (je->stats.luts_inner / S + je->stats.luts_outer / (S * it));
+      g_cells_imad += words * ((je->stats.imads_inner + je->stats.derived_inner) / S +
+                               (je->stats.imads_outer + je->stats.derived_outer) / (S * it));
+    }
     js << (k ? ", " : "") << "{\"variant\": \"" << (sg.generic ? "generic" : "specialised") << "\", \"words\": "
        << (sg.we - sg.wb) << ", \"s\": " << spec.slot_bits << ", \"t\": " << spec.thread_bits
        << ", \"m\": " << spec.inner_bits << ", \"grid\": " << grid << ", \"block\": " << T
@@ -550,7 +564,151 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
        << ", \"thread_vars\": " << je->stats.thread_vars
        << ", \"roles\": \"" << (spec.perm.empty() ? "identity" : "searched") << "\"}";
   }
-  js << "], \"kernels\": " << kernels << "}";
+  js << "], \"kernels\": " << kernels << ", \"cells_lop3\": " << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad
+     << "}";
+  g_last_launch = js.str();
+  return BFA_OK;
+}
+
+void fill_info(bfa_prog* p) {
+  bfa_info& I = p->info;
+  const bfa::Parsed& P = p->parsed;
+  I.max_var_id = P.max_var;
+  I.tree_nodes = P.tree_nodes;
+  I.lets = P.lets;
+  I.support = (uint32_t)__builtin_popcountll(P.support_mask);
+  // G and L over the cone of the root
+  {
+    const bfa::Dag& d = P.dag;
+    std::vector<uint8_t> seen(d.nodes.size(), 0);
+    std::vector<uint32_t> st{bfa::lit_node(P.root)};
+    uint32_t g = 0;
+    uint64_t live_support = 0;
+    while (!st.empty()) {
+      uint32_t n = st.back(); st.pop_back();
+      if (seen[n]) continue;
+      seen[n] = 1;
+      const bfa::Node& nd = d.nodes[n];
+      if (nd.kind == bfa::NK_GATE) { g++; st.push_back(nd.a); st.push_back(nd.b); }
+      if (nd.kind == bfa::NK_VAR) live_support |= 1ull << nd.val;
+    }
+    I.gates = g;
+    (void)live_support;
+    I.const_value = d.nodes[bfa::lit_node(P.root)].kind == bfa::NK_CONST ? (bfa::lit_neg(P.root) ? 1 : 0) : -1;
+    uint32_t L = 0;
+    bfa::dump_ir(P, &L);
+    I.luts = L;
+  }
+}
+
+// Compile (host) the count kernel a whole-range count of p over n variables
+// would launch (plan + role search + NVRTC), without a device.
+int prepare_count(const bfa_prog* p, int n, int sms) {
+  const Options& o = p->opt;
+  if (n < 5 || o.force_generic || o.engine || o.segment_cells || p->info.luts > 8000) return BFA_OK;
+  const int T = 1 << o.thread_bits;
+  const int full_grid = sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
+  const uint64_t whi = 1ull << (n - 5);
+  for (const Segment& sg : plan(o, o.slot_bits, n, 0, whi, full_grid)) {
+    if (sg.generic) continue;
+    bfa::KernelSpec spec;
+    spec.mode = bfa::KM_COUNT; spec.generic = false; spec.slot_bits = o.slot_bits; spec.thread_bits = o.thread_bits;
+    spec.inner_bits = sg.m; spec.dual_pipe = o.dual_pipe; spec.imad_cost_pct = o.imad_cost_pct;
+    spec.min_blocks = o.min_blocks;
+    resolve_roles(p, &spec, aligned_k(sg.wb, sg.we));
+    int rc = get_kernel(p, spec, -1, nullptr, nullptr);
+    if (rc) return rc;
+  }
+  return BFA_OK;
+}
+
+// Count mode entry: with kernel_cofactor_bits = j > 0, an aligned sub-cube of
+// 2^k >= 2^(24+j) valuations is split into 2^j cofactor programs (bfa_assume
+// on the range's fixed top variables and j greedily chosen free ones), each
+// compiled with its own role search and launched in turn, accumulating into
+// one counter (the paper's "further partition").
+int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
+              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
+  const int j = p ? p->opt.kernel_cofactor_bits : 0;
+  if (!p || eval || mu_out || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
+      mu_hi > (1ull << n) || mu_lo >= mu_hi)
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, false);
+  const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
+  if ((mu_lo & 31) || (mu_hi & 31) || k < 24 + j || p->info.luts > 8000 || p->opt.segment_cells)
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, false);
+  if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+  const uint64_t top_vals = mu_lo & top_mask;
+  const std::string key = std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) + "." +
+                          std::to_string(j);
+  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it != mp->cofactors.end()) kids = &it->second;
+  }
+  if (!kids) {
+    // the range's program over its k free variables, then j cofactor variables
+    bfa::Parsed base = bfa::assume(p->parsed, n, top_mask, top_vals, nullptr);
+    std::vector<int> J = bfa::choose_cofactor_vars(base, k, j);
+    uint64_t jmask = 0;
+    for (int v : J) jmask |= 1ull << v;
+    std::vector<std::unique_ptr<bfa_prog>> made;
+    for (uint64_t c = 0; c < (1ull << J.size()); c++) {
+      uint64_t vals = 0;
+      for (size_t b = 0; b < J.size(); b++) vals |= ((c >> b) & 1) << J[b];
+      auto q = std::make_unique<bfa_prog>();
+      q->parsed = bfa::assume(base, k, jmask, vals, nullptr);
+      q->opt = p->opt;
+      q->opt.kernel_cofactor_bits = 0;
+      fill_info(q.get());
+      made.push_back(std::move(q));
+    }
+    const int kk = k - (int)J.size();
+    {  // compile every child's kernel in parallel (host only)
+      std::vector<std::thread> th;
+      std::vector<int> rcs(made.size(), 0);
+      for (size_t i = 0; i < made.size(); i++)
+        th.emplace_back([&, i] { rcs[i] = prepare_count(made[i].get(), kk, di.sms); });
+      for (auto& t : th) t.join();
+      for (int r : rcs) if (r) return r;
+    }
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
+    kids = &it->second;
+  }
+  cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+  if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  const int kk = k - __builtin_ctzll((unsigned long long)kids->size());
+  int kernels = 0, zero = 0, one = 0;
+  std::string first;
+  double l3 = 0, im = 0;
+  for (auto& q : *kids) {
+    // a cofactor the Reduction proved identically 0 has no models: decided at
+    // compile time, no launch (constant-1 cofactors are launched and counted)
+    if (q->info.const_value == 0) { zero++; continue; }
+    if (q->info.const_value == 1) one++;
+    g_cells_lop3 = g_cells_imad = 0;
+    rc = run_range_core(q.get(), kk, 0, 1ull << kk, nullptr, count_dev, st, false, -1, nullptr, 0, true);
+    if (rc) return rc;
+    l3 += g_cells_lop3;
+    im += g_cells_imad;
+    kernels++;
+    if (first.empty()) first = g_last_launch;
+  }
+  g_cells_lop3 = l3;
+  g_cells_imad = im;
+  std::ostringstream js;
+  js << "{\"variant\": \"kernel-cofactored\", \"cofactors\": " << kids->size() << ", \"constant_zero\": " << zero
+     << ", \"constant_one\": " << one << ", \"valuations_per_cofactor\": " << (1ull << kk)
+     << ", \"kernels\": " << kernels << ", \"cells_lop3\": " << l3 << ", \"cells_imad\": " << im
+     << ", \"first\": " << (first.empty() ? "{}" : first) << "}";
   g_last_launch = js.str();
   return BFA_OK;
 }
@@ -610,37 +768,6 @@ extern "C" {
 
 const char* bfa_last_error(void) { return g_err.c_str(); }
 const char* bfa_version(void) { return "bfa 0.1 (sm_100a; NVRTC static)"; }
-
-static void fill_info(bfa_prog* p) {
-  bfa_info& I = p->info;
-  const bfa::Parsed& P = p->parsed;
-  I.max_var_id = P.max_var;
-  I.tree_nodes = P.tree_nodes;
-  I.lets = P.lets;
-  I.support = (uint32_t)__builtin_popcountll(P.support_mask);
-  // G and L over the cone of the root
-  {
-    const bfa::Dag& d = P.dag;
-    std::vector<uint8_t> seen(d.nodes.size(), 0);
-    std::vector<uint32_t> st{bfa::lit_node(P.root)};
-    uint32_t g = 0;
-    uint64_t live_support = 0;
-    while (!st.empty()) {
-      uint32_t n = st.back(); st.pop_back();
-      if (seen[n]) continue;
-      seen[n] = 1;
-      const bfa::Node& nd = d.nodes[n];
-      if (nd.kind == bfa::NK_GATE) { g++; st.push_back(nd.a); st.push_back(nd.b); }
-      if (nd.kind == bfa::NK_VAR) live_support |= 1ull << nd.val;
-    }
-    I.gates = g;
-    (void)live_support;
-    I.const_value = d.nodes[bfa::lit_node(P.root)].kind == bfa::NK_CONST ? (bfa::lit_neg(P.root) ? 1 : 0) : -1;
-    uint32_t L = 0;
-    bfa::dump_ir(P, &L);
-    I.luts = L;
-  }
-}
 
 int bfa_compile(const char* expr, bfa_prog** out) {
   if (!expr || !out) return set_err(BFA_E_ARG, "NULL argument");
@@ -725,6 +852,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "role_budget") { if (v < 1 || v > 4096) return bad(); p->opt.role_budget = (int)v; }
   else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }
   else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
+  else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -865,11 +993,41 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     cands[i].regs = e ? e->regs : 0;
     if (best < 0 || cands[i].ms < cands[best].ms) best = (int)i;
   }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   cudaError_t ce = cudaStreamSynchronize(st);
   if (ce != cudaSuccess) { p->opt = base; return set_err(BFA_E_CUDA, "autotune: %s", cudaGetErrorString(ce)); }
   p->opt = best >= 0 ? cands[best].o : base;
+  // phase 3: kernel-level cofactoring (count mode over the whole sub-cube the
+  // caller will count: 2^k_free valuations when that takes <= ~2 s, else the
+  // probe).  Each j splits into 2^j cofactor programs (prepared once, cached).
+  std::vector<std::pair<int, float>> kcof;
+  if (best >= 0 && k_free >= 28) {
+    const double est = cands[best].ms * std::pow(2.0, k_free - k);
+    uint64_t tlo = lo, thi = hi;
+    if (est <= 2000.0 && k_free == n) { tlo = 0; thi = hi; }
+    else if (est <= 2000.0) { thi = hi; tlo = hi - (1ull << k_free); }
+    int best_j = 0;
+    float best_ms = 1e30f;
+    for (int jj : {0, 2, 4, 6}) {
+      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj) continue;
+      p->opt.kernel_cofactor_bits = jj;
+      if ((rc = run_range(p, n, tlo, thi, nullptr, d, st, false))) { p->opt = cands[best].o; break; }
+      float bm = 1e30f;
+      for (int r = 0; r < 2; r++) {
+        cudaEventRecord(e0, st);
+        run_range(p, n, tlo, thi, nullptr, d, st, false);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        bm = std::min(bm, ms);
+      }
+      kcof.push_back({jj, bm});
+      if (bm < best_ms) { best_ms = bm; best_j = jj; }
+    }
+    p->opt.kernel_cofactor_bits = best_j;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
   js << "{\"probe_valuations\": " << (hi - lo) << ", \"k_free\": " << k_free << ", \"candidates\": [";
   bool first = true;
   for (size_t i = 0; i < cands.size(); i++) {
@@ -882,7 +1040,11 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   }
   js << "], \"best\": {\"slot_bits\": " << p->opt.slot_bits << ", \"inner_bits\": " << p->opt.inner_bits
      << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
-     << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits << "}}";
+     << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits
+     << ", \"kernel_cofactor_bits\": " << p->opt.kernel_cofactor_bits << "}, \"kernel_cofactoring\": [";
+  for (size_t i = 0; i < kcof.size(); i++)
+    js << (i ? ", " : "") << "{\"j\": " << kcof[i].first << ", \"ms\": " << kcof[i].second << "}";
+  js << "]}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
   return BFA_OK;
 }

@@ -246,6 +246,34 @@ def test_role_search_subcubes():
         assert a + b == 1 << k
 
 
+def test_kernel_cofactoring():
+    """Kernel-level cofactoring (2^j cofactor programs via bfa_assume, each
+    with its own role search and kernel, constant-0 cofactors decided at
+    compile time) leaves every count unchanged: full cubes, oracle
+    sub-cubes, and f / ~f summing to the cube."""
+    text, n, expect = W.config("c4")
+    for j in (1, 3, 5):
+        p = bfa.Program(text).set_option("kernel_cofactor_bits", j)
+        assert p.count(n) == expect
+        assert bfa.last_launch()["variant"] == "kernel-cofactored"
+    refl = sum(1 << (35 - 7 * i) for i in range(6))
+    lo = refl & ~((1 << 28) - 1)
+    p = bfa.Program(text).set_option("kernel_cofactor_bits", 3)
+    assert int(p.count_range(n, lo, lo + (1 << 28)).item()) == oracle.count(text, n, lo, lo + (1 << 28))
+    text, n, _ = W.config("c5")
+    body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+    for j in (2, 5):
+        p = bfa.Program(text).set_option("kernel_cofactor_bits", j)
+        pc = bfa.Program(f"{body}\n~{out}").set_option("kernel_cofactor_bits", j)
+        lo = 9 << 30
+        a = int(p.count_range(n, lo, lo + (1 << 30)).item())
+        assert a == int(bfa.Program(text).count_range(n, lo, lo + (1 << 30)).item())
+        assert a + int(pc.count_range(n, lo, lo + (1 << 30)).item()) == 1 << 30
+    lo = 77 << 24
+    p = bfa.Program(text).set_option("kernel_cofactor_bits", 0)
+    assert int(p.count_range(n, lo, lo + (1 << 24)).item()) == oracle.count(text, n, lo, lo + (1 << 24))
+
+
 def test_autotune_keeps_results():
     """bfa_autotune only changes speed: C4 still counts 130023 and a
     sub-cube vector still equals the oracle's after tuning."""
