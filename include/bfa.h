@@ -149,6 +149,14 @@ int bfa_eval(const bfa_prog* p, int n, uint64_t* out);
 int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
                     uint64_t* count_dev, void* stream);
 
+/* Multi-GPU count with work-balanced cofactor sharding (
+ * DESIGN.md §6): every rank derives the same split of the 2^n cube into 2^j
+ * cofactor programs (j >= log2(world) + 2), estimates their work and assigns
+ * them to ranks (longest first); *count_dev (device, written) receives this
+ * rank's share, and the sum over ranks 0..world-1 is bfa_count(p, n).  The
+ * caller sums with one all-reduce.  Synchronous on `stream`. */
+int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, void* stream);
+
 /* The slice [mu_lo, mu_hi) of the DNF vector, asynchronously on `stream`:
  * bit (mu - mu_lo) at word (mu - mu_lo) >> 6 of out_dev (device,
  * ceil((mu_hi-mu_lo)/64) words).  mu_lo, mu_hi multiples of 64, or the whole

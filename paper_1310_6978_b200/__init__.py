@@ -50,6 +50,7 @@ _SIGS = {
     "bfa_batch_create": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(_c.c_void_p)]),
     "bfa_batch_count": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int), _c.c_void_p, _c.c_void_p]),
     "bfa_batch_free": (None, [_c.c_void_p]),
+    "bfa_count_shard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -172,6 +173,13 @@ class Program:
         """bfa_count_range: models in [lo, hi) into a 1-element device tensor (async)."""
         out = _u64_out(out, 1)
         _check(_load().bfa_count_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+        return out
+
+    def count_shard(self, n: int, rank: int, world: int, out=None, stream=None):
+        """bfa_count_shard: this rank's share of the count under work-balanced
+        cofactor sharding (sum over ranks = count(n))."""
+        out = _u64_out(out, 1)
+        _check(_load().bfa_count_shard(self._h, n, rank, world, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
         return out
 
     def eval(self, n: int, out=None):

@@ -313,6 +313,13 @@ cudaError_t sort_u64(uint64_t* keys, uint64_t n, int end_bit, cudaStream_t st) {
   return e;
 }
 
+__global__ void add_u64_kernel(u64* dst, const u64* src) { *dst += *src; }
+
+cudaError_t add_u64(uint64_t* dst, const uint64_t* src, cudaStream_t st) {
+  add_u64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<u64*>(dst), reinterpret_cast<const u64*>(src));
+  return cudaGetLastError();
+}
+
 cudaError_t peak_int(int op, int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st) {
   if (op == 0) peak_lop3_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);
   else if (op == 1) peak_imad_kernel<<<blocks, threads, 0, st>>>(sink, iters, 0x1234567u);

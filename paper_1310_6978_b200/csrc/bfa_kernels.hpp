@@ -17,6 +17,8 @@ cudaError_t interp(const uint32_t* ops, int n_ops, const uint32_t* consts, int n
                    uint64_t* count, cudaStream_t st, int* block_used);
 // ascending radix sort of n u64 keys in place (bits [0, end_bit))
 cudaError_t sort_u64(uint64_t* keys, uint64_t n, int end_bit, cudaStream_t st);
+// *dst += *src on the device
+cudaError_t add_u64(uint64_t* dst, const uint64_t* src, cudaStream_t st);
 // op 0: lop3.b32, 1: mad.lo.u32, 2: both 1:1 -- 256 ops per thread per iteration
 cudaError_t peak_int(int op, int blocks, int threads, int iters, uint32_t* sink, cudaStream_t st);
 }  // namespace bfa_k

@@ -40,6 +40,9 @@ thread_local std::string g_last_launch = "{}";
 // executed integer cells (LOP3 + IMAD + IMAD operand registers) of the last
 // launch sequence, split by pipe; the bench's roofline numerator
 thread_local double g_cells_lop3 = 0, g_cells_imad = 0;
+// valuations of the last count decided at compile time (cofactors/pieces
+// the Reduction proved identically 0, so no kernel ran over them)
+thread_local double g_decided = 0;
 
 int set_err(int code, const char* fmt, ...) {
   char buf[2048];
@@ -160,6 +163,7 @@ struct Options {
   int segment_cells = 0;   // 0: auto (segment when L > 8000), > 0: always, this many cells
   int segment_remat = 2;   // recompute shared cells with cones <= this many cells
   int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
+  int split_pieces = 0;          // count: Shannon-decompose aligned sub-cubes into this many pieces first
 };
 
 struct JitEntry {
@@ -183,6 +187,7 @@ struct bfa_prog {
   std::map<std::string, std::vector<int8_t>> roles;  // role-search results
   std::map<std::string, std::unique_ptr<bfa::SegPlan>> segplans;
   std::map<std::string, std::vector<std::unique_ptr<bfa_prog>>> cofactors;  // kernel-level cofactoring
+  int piece_nv = -1;  // a sharding piece: its number of free variables
 };
 
 namespace {
@@ -371,6 +376,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
 
   cudaError_t ce;
   if (!accumulate) g_cells_lop3 = g_cells_imad = 0;
+  if (!accumulate) g_decided = 0;
   if (count_dev && !accumulate) {
     ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
     if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
@@ -627,8 +633,16 @@ int prepare_count(const bfa_prog* p, int n, int sms) {
 // on the range's fixed top variables and j greedily chosen free ones), each
 // compiled with its own role search and launched in turn, accumulating into
 // one counter (the paper's "further partition").
+int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st);
+
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
               cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
+  if (p && !eval && !mu_out && force_roles_k < 0 && p->opt.split_pieces > 1 && n <= 63 && p->info.max_var_id < n &&
+      mu_hi <= (1ull << n) && mu_lo < mu_hi && !(mu_lo & 31) && !(mu_hi & 31) && count_dev &&
+      p->info.luts <= 8000 && !p->opt.segment_cells) {
+    const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
+    if (k >= 30) return decompose_count(p, n, mu_lo, k, count_dev, st);
+  }
   const int j = p ? p->opt.kernel_cofactor_bits : 0;
   if (!p || eval || mu_out || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
       mu_hi > (1ull << n) || mu_lo >= mu_hi)
@@ -704,11 +718,230 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   }
   g_cells_lop3 = l3;
   g_cells_imad = im;
+  g_decided = (double)zero * (double)(1ull << kk);
   std::ostringstream js;
   js << "{\"variant\": \"kernel-cofactored\", \"cofactors\": " << kids->size() << ", \"constant_zero\": " << zero
+     << ", \"valuations_decided\": " << g_decided
      << ", \"constant_one\": " << one << ", \"valuations_per_cofactor\": " << (1ull << kk)
      << ", \"kernels\": " << kernels << ", \"cells_lop3\": " << l3 << ", \"cells_imad\": " << im
      << ", \"first\": " << (first.empty() ? "{}" : first) << "}";
+  g_last_launch = js.str();
+  return BFA_OK;
+}
+
+// Work-balanced cofactor sharding (multi-GPU count).  Every rank derives the
+// same decomposition of the 2^n cube: starting from the whole program, the
+// heaviest non-constant piece (work = (gates + 1) x 2^free_vars) is split by
+// its own best variable (both cofactors via bfa_assume + Reduction) until
+// there are >= 4 non-constant pieces per rank; pieces the Reduction proves 0
+// have no work.  Pieces go to ranks by LPT (heaviest first to the least
+// loaded rank, deterministic ties).  A rank counts only its pieces; the sum
+// over ranks is the full count.
+int scratch_u64(int dev, uint64_t** p);
+
+struct Piece {
+  std::unique_ptr<bfa_prog> prog;
+  int nv = 0;
+  uint64_t work = 0;
+};
+
+static uint64_t piece_work(const bfa_prog* q, int nv) {
+  if (q->info.const_value == 0) return 0;
+  return (uint64_t)(q->info.gates + 1) << std::min(nv, 40);
+}
+
+// Shannon decomposition of `base` (nv free variables): split the heaviest
+// non-constant piece by its own best variable until `target` non-constant
+// pieces exist (or no piece has more than 24 variables).  Pieces inherit p's
+// options (incl. kernel_cofactor_bits, applied inside each piece).
+std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed base, int nv, int target) {
+  std::vector<Piece> pieces;
+  {
+    Piece root;
+    root.prog = std::make_unique<bfa_prog>();
+    root.prog->parsed = std::move(base);
+    root.prog->opt = p->opt;
+    fill_info(root.prog.get());
+    root.nv = nv;
+    root.work = piece_work(root.prog.get(), nv);
+    pieces.push_back(std::move(root));
+  }
+  auto nonconst = [&] { int c = 0; for (auto& x : pieces) c += x.work > 0; return c; };
+  for (int guard = 0; guard < 4096 && nonconst() < target; guard++) {
+    size_t h = pieces.size();
+    for (size_t i = 0; i < pieces.size(); i++)
+      if (pieces[i].work > 0 && pieces[i].nv > 24 && (h == pieces.size() || pieces[i].work > pieces[h].work)) h = i;
+    if (h == pieces.size()) break;
+    Piece big = std::move(pieces[h]);
+    pieces.erase(pieces.begin() + h);
+    std::vector<int> J = bfa::choose_cofactor_vars(big.prog->parsed, big.nv, 1);
+    const int v = J.empty() ? 0 : J[0];
+    for (int b = 0; b < 2; b++) {
+      Piece c;
+      c.prog = std::make_unique<bfa_prog>();
+      c.prog->parsed = bfa::assume(big.prog->parsed, big.nv, 1ull << v, (uint64_t)b << v, nullptr);
+      c.prog->opt = p->opt;
+      fill_info(c.prog.get());
+      c.nv = big.nv - 1;
+      c.work = piece_work(c.prog.get(), c.nv);
+      pieces.insert(pieces.begin() + h + b, std::move(c));
+    }
+  }
+  std::vector<std::unique_ptr<bfa_prog>> made;
+  for (auto& x : pieces) {
+    x.prog->opt.split_pieces = 0;
+    x.prog->piece_nv = x.nv;
+    made.push_back(std::move(x.prog));
+  }
+  return made;
+}
+
+// Count the pieces owned by `rank` (owner[i] == rank) into count_dev (written).
+int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
+                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out);
+
+int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, cudaStream_t st,
+                std::string* report) {
+  if (world < 1 || rank < 0 || rank >= world) return set_err(BFA_E_ARG, "rank %d of %d", rank, world);
+  if (n < 0 || n > 63 || p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "bad n=%d", n);
+  if (world == 1 || n < 26) {
+    if (rank != 0) return cudaMemsetAsync(count_dev, 0, 8, st) == cudaSuccess ? BFA_OK : set_err(BFA_E_CUDA, "memset");
+    return run_range(p, n, 0, n == 63 ? (1ull << 63) : (1ull << n), nullptr, count_dev, st, false);
+  }
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  const std::string key = "shard." + std::to_string(n) + "." + std::to_string(world);
+  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it != mp->cofactors.end()) kids = &it->second;
+  }
+  if (!kids) {
+    std::vector<std::unique_ptr<bfa_prog>> made =
+        decompose(p, bfa::assume(p->parsed, n, 0, 0, nullptr), n, std::max(4 * world, p->opt.split_pieces));
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
+    kids = &it->second;
+  }
+  // LPT assignment (identical on every rank)
+  std::vector<std::pair<uint64_t, size_t>> work;
+  for (size_t i = 0; i < kids->size(); i++)
+    work.push_back({piece_work((*kids)[i].get(), (*kids)[i]->piece_nv), i});
+  std::stable_sort(work.begin(), work.end(), [](auto& a, auto& b) { return a.first > b.first; });
+  std::vector<uint64_t> load(world, 0);
+  std::vector<int> owner(kids->size(), 0);
+  for (auto& wi : work) {
+    int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
+    owner[wi.second] = r;
+    load[r] += wi.first;
+  }
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  int kernels = 0;
+  if ((rc = count_pieces(*kids, owner, rank, dev, di.sms, count_dev, st, &kernels))) return rc;
+  if (report) {
+    std::ostringstream js;
+    js << "{\"variant\": \"cofactor-sharded\", \"pieces\": " << kids->size() << ", \"valuations_decided\": "
+       << g_decided << ", \"cells_lop3\": " << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad
+       << ", \"rank\": " << rank
+       << ", \"world\": " << world << ", \"kernels\": " << kernels << ", \"load\": [";
+    for (int r = 0; r < world; r++) js << (r ? ", " : "") << load[r];
+    js << "]}";
+    *report = js.str();
+  }
+  return BFA_OK;
+}
+
+int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
+                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out) {
+  cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+  if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  {  // compile the owned pieces' kernels in parallel (pieces that split
+     // further into cofactor kernels prepare their own children)
+    std::vector<std::thread> th;
+    std::vector<int> rcs(kids.size(), 0);
+    for (size_t i = 0; i < kids.size(); i++)
+      if (owner[i] == rank && kids[i]->info.const_value != 0 && kids[i]->opt.kernel_cofactor_bits == 0)
+        th.emplace_back([&, i] { rcs[i] = prepare_count(kids[i].get(), kids[i]->piece_nv, sms); });
+    for (auto& t : th) t.join();
+    for (int r : rcs) if (r) return r;
+  }
+  // unsplit pieces accumulate straight into count_dev; a piece that splits
+  // into its own cofactor kernels counts into a scratch word that a 1-thread
+  // kernel then adds to count_dev (stream order keeps the scratch reusable)
+  uint64_t* tmp = nullptr;
+  int rc = scratch_u64(dev, &tmp);  // 8 words: [0] is bfa_count's result, [4] this temporary
+  if (rc) return rc;
+  tmp += 4;
+  if (tmp == count_dev) return set_err(BFA_E_ARG, "count buffer aliases the library scratch");
+  int kernels = 0;
+  double l3 = 0, im = 0, decided = 0;
+  for (size_t i = 0; i < kids.size(); i++) {
+    if (owner[i] != rank) continue;
+    const int nv = kids[i]->piece_nv;
+    if (kids[i]->info.const_value == 0) { decided += (double)(1ull << nv); continue; }
+    g_cells_lop3 = g_cells_imad = 0;
+    g_decided = 0;
+    if (kids[i]->opt.kernel_cofactor_bits > 0) {
+      rc = run_range(kids[i].get(), nv, 0, 1ull << nv, nullptr, tmp, st, false);
+      if (!rc) rc = bfa_k::add_u64(count_dev, tmp, st) == cudaSuccess ? BFA_OK : set_err(BFA_E_CUDA, "add");
+    } else {
+      rc = run_range_core(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, st, false, -1, nullptr, 0, true);
+    }
+    if (rc) return rc;
+    l3 += g_cells_lop3;
+    im += g_cells_imad;
+    decided += g_decided;
+    kernels++;
+  }
+  g_cells_lop3 = l3;
+  g_cells_imad = im;
+  g_decided = decided;
+  if (kernels_out) *kernels_out = kernels;
+  return BFA_OK;
+}
+
+// Single-device count of an aligned sub-cube through a Shannon
+// decomposition into split_pieces pieces (each with its own kernel-level
+// cofactoring); pieces are prepared once and cached.
+int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st) {
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+  const uint64_t top_vals = mu_lo & top_mask;
+  const std::string key = "split." + std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) +
+                          "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits);
+  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it != mp->cofactors.end()) kids = &it->second;
+  }
+  if (!kids) {
+    std::vector<std::unique_ptr<bfa_prog>> made =
+        decompose(p, bfa::assume(p->parsed, n, top_mask, top_vals, nullptr), k, p->opt.split_pieces);
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
+    kids = &it->second;
+  }
+  std::vector<int> owner(kids->size(), 0);
+  int kernels = 0, zero = 0;
+  uint64_t zero_vals = 0;
+  for (auto& q : *kids)
+    if (q->info.const_value == 0) { zero++; zero_vals += 1ull << q->piece_nv; }
+  if ((rc = count_pieces(*kids, owner, 0, dev, di.sms, count_dev, st, &kernels))) return rc;
+  std::ostringstream js;
+  (void)zero_vals;
+  js << "{\"variant\": \"decomposed\", \"pieces\": " << kids->size() << ", \"constant_zero\": " << zero
+     << ", \"valuations_decided\": " << g_decided << ", \"kernels\": " << kernels << ", \"cells_lop3\": "
+     << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad << "}";
   g_last_launch = js.str();
   return BFA_OK;
 }
@@ -777,6 +1010,14 @@ int bfa_compile(const char* expr, bfa_prog** out) {
   fill_info(p.get());
   *out = p.release();
   return BFA_OK;
+}
+
+int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, void* stream) {
+  if (!p || !count_dev) return set_err(BFA_E_ARG, "NULL argument");
+  std::string rep;
+  int rc = count_shard(p, n, rank, world, count_dev, (cudaStream_t)stream, &rep);
+  if (rc == BFA_OK && !rep.empty()) g_last_launch = rep;
+  return rc;
 }
 
 int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_prog** out, int* n_free,
@@ -853,6 +1094,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }
   else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
   else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }
+  else if (k == "split_pieces") { if (v < 0 || v > 1024) return bad(); p->opt.split_pieces = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -1005,11 +1247,15 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     uint64_t tlo = lo, thi = hi;
     if (est <= 2000.0 && k_free == n) { tlo = 0; thi = hi; }
     else if (est <= 2000.0) { thi = hi; tlo = hi - (1ull << k_free); }
-    int best_j = 0;
+    int best_j = 0, best_sp = 0;
     float best_ms = 1e30f;
-    for (int jj : {0, 2, 4, 6}) {
-      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj) continue;
+    std::vector<std::pair<int, int>> trials = {{0, 0}, {0, 2}, {0, 4}, {0, 6}, {8, -1}, {16, -2}};
+    for (auto tr : trials) {
+      int sp = tr.first, jj = tr.second;
+      if (jj < 0) jj = std::max(0, best_j + jj + 1);  // relative to the best j so far
+      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj + (sp ? 4 : 0)) continue;
       p->opt.kernel_cofactor_bits = jj;
+      p->opt.split_pieces = sp;
       if ((rc = run_range(p, n, tlo, thi, nullptr, d, st, false))) { p->opt = cands[best].o; break; }
       float bm = 1e30f;
       for (int r = 0; r < 2; r++) {
@@ -1021,10 +1267,11 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
         cudaEventElapsedTime(&ms, e0, e1);
         bm = std::min(bm, ms);
       }
-      kcof.push_back({jj, bm});
-      if (bm < best_ms) { best_ms = bm; best_j = jj; }
+      kcof.push_back({jj + 100 * sp, bm});
+      if (bm < best_ms) { best_ms = bm; best_j = jj; best_sp = sp; }
     }
     p->opt.kernel_cofactor_bits = best_j;
+    p->opt.split_pieces = best_sp;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -1041,9 +1288,11 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   js << "], \"best\": {\"slot_bits\": " << p->opt.slot_bits << ", \"inner_bits\": " << p->opt.inner_bits
      << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
      << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits
-     << ", \"kernel_cofactor_bits\": " << p->opt.kernel_cofactor_bits << "}, \"kernel_cofactoring\": [";
+     << ", \"kernel_cofactor_bits\": " << p->opt.kernel_cofactor_bits << ", \"split_pieces\": " << p->opt.split_pieces
+     << "}, \"kernel_cofactoring\": [";
   for (size_t i = 0; i < kcof.size(); i++)
-    js << (i ? ", " : "") << "{\"j\": " << kcof[i].first << ", \"ms\": " << kcof[i].second << "}";
+    js << (i ? ", " : "") << "{\"split_pieces\": " << kcof[i].first / 100 << ", \"j\": " << kcof[i].first % 100
+       << ", \"ms\": " << kcof[i].second << "}";
   js << "]}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
   return BFA_OK;

@@ -27,20 +27,26 @@ def rank_range(n: int, rank: int, world: int):
     return rank * span, (rank + 1) * span
 
 
-def count_sharded(prog, n: int, group=None, count_range=None, stream=None):
+def count_sharded(prog, n: int, group=None, count_range=None, stream=None, balanced: bool = True):
     """Model count over all 2^n valuations, sharded over the process group.
 
     Returns a 1-element int64 tensor holding the global count on every rank.
-    `count_range(n, lo, hi)` defaults to prog.count_range (the GPU path); the
-    CPU multi-process tests inject another range counter to exercise the
-    partition and the reduction with the gloo backend."""
+    balanced (GPU path): each rank counts the cofactors bfa_count_shard
+    assigns it (work-balanced LPT over a deterministic cofactor split, no
+    rank-range specialisation imbalance).  Otherwise rank r counts its
+    contiguous range rank_range(n, r, P) with `count_range(n, lo, hi)`
+    (default prog.count_range); the CPU multi-process tests inject another
+    range counter to exercise the partition and the reduction with gloo."""
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
-    lo, hi = rank_range(n, rank, world)
-    if count_range is None:
+    if count_range is None and balanced:
+        t = prog.count_shard(n, rank, world, stream=stream)
+    elif count_range is None:
+        lo, hi = rank_range(n, rank, world)
         t = prog.count_range(n, lo, hi, stream=stream)
     else:
+        lo, hi = rank_range(n, rank, world)
         t = count_range(n, lo, hi)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)

@@ -274,6 +274,40 @@ def test_kernel_cofactoring():
     assert int(p.count_range(n, lo, lo + (1 << 24)).item()) == oracle.count(text, n, lo, lo + (1 << 24))
 
 
+def test_split_pieces():
+    """Shannon decomposition into pieces (each with kernel-level
+    cofactoring) leaves counts unchanged, on the full cube and on an aligned
+    sub-cube."""
+    for cfg in ("c4", "c5"):
+        text, n, _ = W.config(cfg)
+        full = bfa.Program(text).count(n)
+        for sp, j in ((8, 0), (8, 4), (16, 2)):
+            p = bfa.Program(text).set_option("split_pieces", sp).set_option("kernel_cofactor_bits", j)
+            assert p.count(n) == full, (cfg, sp, j)              # bfa_count (host result)
+            assert int(p.count_range(n, 0, 1 << n).item()) == full
+            assert bfa.last_launch()["variant"] == "decomposed"
+    text, n, _ = W.config("c5")
+    lo = 5 << 32
+    p = bfa.Program(text).set_option("split_pieces", 8).set_option("kernel_cofactor_bits", 2)
+    assert int(p.count_range(n, lo, lo + (1 << 32)).item()) == \
+        int(bfa.Program(text).count_range(n, lo, lo + (1 << 32)).item())
+
+
+def test_count_shard_sums_to_count():
+    """Work-balanced cofactor sharding (bfa_count_shard): the ranks' shares,
+    computed here one after another in one process, sum to the full count for
+    P = 2, 4, 8; the LPT loads are balanced."""
+    for cfg in ("c4", "c5"):
+        text, n, _ = W.config(cfg)
+        full = bfa.Program(text).count(n)
+        p = bfa.Program(text)
+        for world in (2, 4, 8):
+            shares = [int(p.count_shard(n, r, world).item()) for r in range(world)]
+            assert sum(shares) == full, (cfg, world, shares)
+            load = bfa.last_launch()["load"]
+            assert len(load) == world and max(load) <= 1.6 * sum(load) / world, (cfg, world, load)
+
+
 def test_autotune_keeps_results():
     """bfa_autotune only changes speed: C4 still counts 130023 and a
     sub-cube vector still equals the oracle's after tuning."""
