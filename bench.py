@@ -50,6 +50,9 @@ def parse_args():
     ap.add_argument("--config", default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--options", default=None,
+                    help="JSON dict of program options: skip autotuning (e.g. to profile the exact "
+                         "configuration an earlier plain run chose)")
     return ap.parse_args()
 
 
@@ -239,7 +242,10 @@ def run_bfa(args):
     # same kernel.  The one-time preparation cost (tuning, role search,
     # cofactor split, NVRTC) is reported as jit_prep_s.
     t_prep = time.perf_counter()
-    tune = prog.autotune(n) if rank == 0 else None
+    if args.options:
+        tune = {"best": json.loads(args.options), "source": "--options"}
+    else:
+        tune = prog.autotune(n) if rank == 0 else None
     if world > 1:
         obj = [tune]
         dist.broadcast_object_list(obj, src=0)
@@ -263,6 +269,7 @@ def run_bfa(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
+    launches0 = bfa.last_launch().get("launch_counter", 0)
     clocks.start()
     time.sleep(0.3)
     for i in range(args.steps):
@@ -275,6 +282,7 @@ def run_bfa(args):
             dist.all_reduce(cnt)
         ends[i].record(stream)
     torch.cuda.synchronize()
+    launches_timed = bfa.last_launch().get("launch_counter", 0) - launches0
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -365,7 +373,7 @@ def run_bfa(args):
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
                 "call": "bfa_count(prog, n) -> host uint64"},
-        "gpu_launches": kernels_per_step * args.steps,
+        "gpu_launches": launches_timed,
         "kernel_ms_per_step": kernel_s * 1e3,
         "launch": launch,
         "autotune": tune,

@@ -43,6 +43,54 @@ thread_local double g_cells_lop3 = 0, g_cells_imad = 0;
 // valuations of the last count decided at compile time (cofactors/pieces
 // the Reduction proved identically 0, so no kernel ran over them)
 thread_local double g_decided = 0;
+// kernel launches of this library on this thread (monotonic)
+thread_local uint64_t g_launches = 0;
+// nested multi-launch counts add into their caller's counter (no memset)
+thread_local bool g_accumulate = false;
+// inside a fork: nested loops keep their single stream
+thread_local bool g_forked = false;
+
+// Fork/join of independent launches over side streams (their counts only
+// meet in atomics), so short kernels overlap instead of idling SMs during
+// each other's tails; capturable into a CUDA graph as parallel branches.
+struct Fork {
+  static constexpr int K = 4;
+  cudaStream_t base = nullptr;
+  bool active = false;
+  int next = 0;
+  struct Pool { cudaStream_t s[K] = {}; cudaEvent_t ev[K + 1] = {}; bool ok = false; };
+  static Pool& pool(int dev) {
+    static thread_local std::map<int, Pool> pools;
+    Pool& pl = pools[dev];
+    if (!pl.ok) {
+      pl.ok = true;
+      for (int i = 0; i < K; i++) pl.ok &= cudaStreamCreateWithFlags(&pl.s[i], cudaStreamNonBlocking) == cudaSuccess;
+      for (int i = 0; i <= K; i++) pl.ok &= cudaEventCreateWithFlags(&pl.ev[i], cudaEventDisableTiming) == cudaSuccess;
+    }
+    return pl;
+  }
+  Pool* pl = nullptr;
+  Fork(cudaStream_t st, int dev) : base(st) {
+    if (g_forked) return;
+    pl = &pool(dev);
+    if (!pl->ok) return;
+    if (cudaEventRecord(pl->ev[K], st) != cudaSuccess) return;
+    for (int i = 0; i < K; i++) cudaStreamWaitEvent(pl->s[i], pl->ev[K], 0);
+    active = true;
+    g_forked = true;
+  }
+  cudaStream_t stream() { return active ? pl->s[next++ % K] : base; }
+  void join() {
+    if (!active) return;
+    for (int i = 0; i < K; i++) {
+      cudaEventRecord(pl->ev[i], pl->s[i]);
+      cudaStreamWaitEvent(base, pl->ev[i], 0);
+    }
+    active = false;
+    g_forked = false;
+  }
+  ~Fork() { join(); }
+};
 
 int set_err(int code, const char* fmt, ...) {
   char buf[2048];
@@ -164,6 +212,7 @@ struct Options {
   int segment_remat = 2;   // recompute shared cells with cones <= this many cells
   int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
   int split_pieces = 0;          // count: Shannon-decompose aligned sub-cubes into this many pieces first
+  int graphs = 1;                // replay multi-launch counts as CUDA graphs
 };
 
 struct JitEntry {
@@ -188,6 +237,13 @@ struct bfa_prog {
   std::map<std::string, std::unique_ptr<bfa::SegPlan>> segplans;
   std::map<std::string, std::vector<std::unique_ptr<bfa_prog>>> cofactors;  // kernel-level cofactoring
   int piece_nv = -1;  // a sharding piece: its number of free variables
+  // CUDA graphs of multi-launch counts: key -> (calls seen, instantiated graph)
+  std::map<std::string, std::pair<int, cudaGraphExec_t>> graphs;
+  std::map<std::string, uint64_t> graph_launches;  // kernels per replay
+  ~bfa_prog() {
+    for (auto& g : graphs)
+      if (g.second.second) cudaGraphExecDestroy(g.second.second);
+  }
 };
 
 namespace {
@@ -316,6 +372,7 @@ int get_kernel_src(const bfa_prog* cp, const std::string& key, const std::string
 }
 
 int launch(CUfunction fn, unsigned grid, unsigned block, cudaStream_t st, void** args) {
+  g_launches++;
   CUresult r = drv().LaunchKernel(fn, grid, 1, 1, block, 1, 1, 0, (CUstream)st, args, nullptr);
   if (r != CUDA_SUCCESS) return set_err(BFA_E_CUDA, "cuLaunchKernel: %s", cu_str(r).c_str());
   return BFA_OK;
@@ -635,8 +692,88 @@ int prepare_count(const bfa_prog* p, int n, int sms) {
 // one counter (the paper's "further partition").
 int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st);
 
+int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
+                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out,
+                     uint64_t cap);
+
+// Multi-launch counts (decomposition / kernel cofactoring) replay as a CUDA
+// graph: the first call runs directly (and prepares every kernel), the second
+// captures the launch sequence on an internal non-blocking stream, later
+// calls launch the instantiated graph on the caller's stream.
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
               cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
+  const bool multi = p && (p->opt.split_pieces > 1 || p->opt.kernel_cofactor_bits > 0);
+  if (!multi || !p->opt.graphs || eval || mu_out || force_roles_k >= 0 || !count_dev)
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const Options& o = p->opt;
+  std::ostringstream k;
+  k << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << "|" << o.slot_bits << ','
+    << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic << ',' << o.engine << ','
+    << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search << ',' << o.role_budget
+    << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ',' << o.split_pieces;
+  const std::string key = k.str();
+  int calls;
+  cudaGraphExec_t exec = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto& e = mp->graphs[key];
+    calls = e.first++;
+    exec = e.second;
+  }
+  if (exec) {
+    cudaError_t e = cudaGraphLaunch(exec, st);
+    if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lk(mp->mu);
+    g_launches += mp->graph_launches[key];
+    return BFA_OK;
+  }
+  if (calls == 0)
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+  // capture on an internal stream ordered after the caller's stream
+  static thread_local std::map<int, cudaStream_t> cap_streams;
+  cudaStream_t cs = cap_streams[dev];
+  if (!cs) {
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+      return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+    cap_streams[dev] = cs;
+  }
+  cudaGraph_t graph = nullptr;
+  const uint64_t l0 = g_launches;
+  cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  int rc = BFA_OK;
+  if (e == cudaSuccess) {
+    rc = run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, cs, eval, force_roles_k, mu_out, cap);
+    e = cudaStreamEndCapture(cs, &graph);
+  }
+  const uint64_t captured = g_launches - l0;
+  g_launches = l0;  // captured, not launched yet
+  if (rc || e != cudaSuccess || !graph) {
+    cudaGetLastError();
+    if (graph) cudaGraphDestroy(graph);
+    std::lock_guard<std::mutex> lk(mp->mu);
+    mp->opt.graphs = 0;  // not capturable here: run directly from now on
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+  }
+  e = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e));
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    mp->graphs[key].second = exec;
+    mp->graph_launches[key] = captured;
+  }
+  e = cudaGraphLaunch(exec, st);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
+  g_launches += captured;
+  return BFA_OK;
+}
+
+int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
+                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out,
+                     uint64_t cap) {
   if (p && !eval && !mu_out && force_roles_k < 0 && p->opt.split_pieces > 1 && n <= 63 && p->info.max_var_id < n &&
       mu_hi <= (1ull << n) && mu_lo < mu_hi && !(mu_lo & 31) && !(mu_hi & 31) && count_dev &&
       p->info.luts <= 8000 && !p->opt.segment_cells) {
@@ -646,10 +783,10 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   const int j = p ? p->opt.kernel_cofactor_bits : 0;
   if (!p || eval || mu_out || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
       mu_hi > (1ull << n) || mu_lo >= mu_hi)
-    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, false);
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, g_accumulate);
   const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
   if ((mu_lo & 31) || (mu_hi & 31) || k < 24 + j || p->info.luts > 8000 || p->opt.segment_cells)
-    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, false);
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, g_accumulate);
   if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
   int dev;
   DevInfo di;
@@ -680,6 +817,8 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
       q->parsed = bfa::assume(base, k, jmask, vals, nullptr);
       q->opt = p->opt;
       q->opt.kernel_cofactor_bits = 0;
+      q->opt.split_pieces = 0;
+      q->opt.graphs = 0;
       fill_info(q.get());
       made.push_back(std::move(q));
     }
@@ -697,25 +836,29 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
     kids = &it->second;
   }
-  cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
-  if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  if (!g_accumulate) {
+    cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+    if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  }
   const int kk = k - __builtin_ctzll((unsigned long long)kids->size());
   int kernels = 0, zero = 0, one = 0;
   std::string first;
   double l3 = 0, im = 0;
+  Fork fork(st, dev);
   for (auto& q : *kids) {
     // a cofactor the Reduction proved identically 0 has no models: decided at
     // compile time, no launch (constant-1 cofactors are launched and counted)
     if (q->info.const_value == 0) { zero++; continue; }
     if (q->info.const_value == 1) one++;
     g_cells_lop3 = g_cells_imad = 0;
-    rc = run_range_core(q.get(), kk, 0, 1ull << kk, nullptr, count_dev, st, false, -1, nullptr, 0, true);
+    rc = run_range_core(q.get(), kk, 0, 1ull << kk, nullptr, count_dev, fork.stream(), false, -1, nullptr, 0, true);
     if (rc) return rc;
     l3 += g_cells_lop3;
     im += g_cells_imad;
     kernels++;
     if (first.empty()) first = g_last_launch;
   }
+  fork.join();
   g_cells_lop3 = l3;
   g_cells_imad = im;
   g_decided = (double)zero * (double)(1ull << kk);
@@ -790,6 +933,7 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
   std::vector<std::unique_ptr<bfa_prog>> made;
   for (auto& x : pieces) {
     x.prog->opt.split_pieces = 0;
+    x.prog->opt.graphs = 0;  // pieces run inside their parent's graph
     x.prog->piece_nv = x.nv;
     made.push_back(std::move(x.prog));
   }
@@ -869,27 +1013,25 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
     for (auto& t : th) t.join();
     for (int r : rcs) if (r) return r;
   }
-  // unsplit pieces accumulate straight into count_dev; a piece that splits
-  // into its own cofactor kernels counts into a scratch word that a 1-thread
-  // kernel then adds to count_dev (stream order keeps the scratch reusable)
-  uint64_t* tmp = nullptr;
-  int rc = scratch_u64(dev, &tmp);  // 8 words: [0] is bfa_count's result, [4] this temporary
-  if (rc) return rc;
-  tmp += 4;
-  if (tmp == count_dev) return set_err(BFA_E_ARG, "count buffer aliases the library scratch");
+  // every piece adds into count_dev (a piece that splits into its own
+  // cofactor kernels accumulates too); pieces run on forked side streams
   int kernels = 0;
   double l3 = 0, im = 0, decided = 0;
+  int rc = BFA_OK;
+  Fork fork(st, dev);
   for (size_t i = 0; i < kids.size(); i++) {
     if (owner[i] != rank) continue;
     const int nv = kids[i]->piece_nv;
     if (kids[i]->info.const_value == 0) { decided += (double)(1ull << nv); continue; }
     g_cells_lop3 = g_cells_imad = 0;
     g_decided = 0;
+    cudaStream_t ps = fork.stream();
     if (kids[i]->opt.kernel_cofactor_bits > 0) {
-      rc = run_range(kids[i].get(), nv, 0, 1ull << nv, nullptr, tmp, st, false);
-      if (!rc) rc = bfa_k::add_u64(count_dev, tmp, st) == cudaSuccess ? BFA_OK : set_err(BFA_E_CUDA, "add");
+      g_accumulate = true;
+      rc = run_range(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, ps, false);
+      g_accumulate = false;
     } else {
-      rc = run_range_core(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, st, false, -1, nullptr, 0, true);
+      rc = run_range_core(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, ps, false, -1, nullptr, 0, true);
     }
     if (rc) return rc;
     l3 += g_cells_lop3;
@@ -897,6 +1039,7 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
     decided += g_decided;
     kernels++;
   }
+  fork.join();
   g_cells_lop3 = l3;
   g_cells_imad = im;
   g_decided = decided;
@@ -1078,6 +1221,9 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out) {
 int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   if (!p || !key) return set_err(BFA_E_ARG, "NULL argument");
   std::lock_guard<std::mutex> lk(p->mu);
+  for (auto& g : p->graphs)
+    if (g.second.second) cudaGraphExecDestroy(g.second.second);
+  p->graphs.clear();
   std::string k(key);
   auto bad = [&]() { return set_err(BFA_E_ARG, "option %s=%lld out of range", key, (long long)v); };
   if (k == "slot_bits") { if (v < 0 || v > 5) return bad(); p->opt.slot_bits = (int)v; }
@@ -1095,6 +1241,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
   else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }
   else if (k == "split_pieces") { if (v < 0 || v > 1024) return bad(); p->opt.split_pieces = (int)v; }
+  else if (k == "graphs") { if (v < 0 || v > 1) return bad(); p->opt.graphs = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -1611,7 +1758,10 @@ int bfa_eval_materialised(const bfa_prog* p, int n, int variant, uint64_t* out_d
 
 int bfa_last_launch_json(char* buf, size_t len) {
   if (!buf || !len) return set_err(BFA_E_ARG, "NULL buffer");
-  snprintf(buf, len, "%s", g_last_launch.c_str());
+  std::string s = g_last_launch;
+  // append the thread's monotonic launch counter
+  if (!s.empty() && s.back() == '}') s = s.substr(0, s.size() - 1) + ", \"launch_counter\": " + std::to_string(g_launches) + "}";
+  snprintf(buf, len, "%s", s.c_str());
   return BFA_OK;
 }
 

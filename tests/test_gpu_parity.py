@@ -293,6 +293,27 @@ def test_split_pieces():
         int(bfa.Program(text).count_range(n, lo, lo + (1 << 32)).item())
 
 
+def test_graph_replay():
+    """Multi-launch counts replay as CUDA graphs from the third call on:
+    results and the launch counter stay exact across direct, captured and
+    replayed calls and across option changes."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text).set_option("split_pieces", 8).set_option("kernel_cofactor_bits", 2)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    counters = []
+    for _ in range(5):
+        p.count_range(n, 0, 1 << n, out=out)
+        torch.cuda.synchronize()
+        assert int(out.item()) == expect
+        counters.append(bfa.last_launch()["launch_counter"])
+    steps = [b - a for a, b in zip(counters, counters[1:])]
+    assert len(set(steps)) == 1 and steps[0] > 0
+    p.set_option("kernel_cofactor_bits", 3)
+    for _ in range(3):
+        p.count_range(n, 0, 1 << n, out=out)
+        assert int(out.item()) == expect
+
+
 def test_count_shard_sums_to_count():
     """Work-balanced cofactor sharding (bfa_count_shard): the ranks' shares,
     computed here one after another in one process, sum to the full count for
