@@ -111,6 +111,8 @@ struct Driver {
   CUresult (*OccupancyMaxActiveBlocksPerMultiprocessor)(int*, CUfunction, int, size_t) = nullptr;
   CUresult (*FuncGetAttribute)(int*, CUfunction_attribute, CUfunction) = nullptr;
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
+  CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
+  CUresult (*CtxGetDevice)(CUdevice*) = nullptr;
   bool ok = false;
   std::string err;
 };
@@ -129,7 +131,9 @@ Driver& drv() {
               get("cuLaunchKernel", (void**)&d.LaunchKernel) &&
               get("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.OccupancyMaxActiveBlocksPerMultiprocessor) &&
               get("cuFuncGetAttribute", (void**)&d.FuncGetAttribute) &&
-              get("cuGetErrorString", (void**)&d.GetErrorString);
+              get("cuGetErrorString", (void**)&d.GetErrorString) &&
+              get("cuCtxGetCurrent", (void**)&d.CtxGetCurrent) &&
+              get("cuCtxGetDevice", (void**)&d.CtxGetDevice);
     d.ok = ok;
     if (!ok) d.err = "CUDA driver entry points unavailable (no driver / no device)";
   });
@@ -155,6 +159,19 @@ int current_device(int* dev, DevInfo* info) {
                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
   e = cudaGetDevice(dev);
   if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+  // Follow the caller's device: torch (its own CUDA runtime) selects the
+  // device by making that device's primary context current in the driver;
+  // this library's runtime must then use the same device.
+  if (drv().ok) {
+    CUcontext ctx = nullptr;
+    CUdevice cd = 0;
+    if (drv().CtxGetCurrent(&ctx) == CUDA_SUCCESS && ctx && drv().CtxGetDevice(&cd) == CUDA_SUCCESS &&
+        (int)cd != *dev) {
+      e = cudaSetDevice((int)cd);
+      if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaSetDevice(%d): %s", (int)cd, cudaGetErrorString(e));
+      *dev = (int)cd;
+    }
+  }
   static std::mutex mu;
   static std::map<int, DevInfo> cache;
   std::lock_guard<std::mutex> lk(mu);
