@@ -295,11 +295,6 @@ def run_bfa(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total, t_kern = tt.tolist()
     final = int(cnt.item()) & ((1 << 64) - 1)
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return
-
     valuations = (1 << n) * args.steps
     value = valuations / t_total
     words_per_launch = ((hi - lo) if world == 1 else (1 << n) // world) >> 5
@@ -340,8 +335,24 @@ def run_bfa(args):
         e2e_value = valuations / (time.perf_counter() - t0)
         assert e2e_count == final
     else:
-        e2e_value = None
-        e2e_count = final
+        # the public multi-GPU call: dist.count_sharded (this rank's share +
+        # the 8-byte all-reduce) and the result read on the host; max over ranks
+        from paper_1310_6978_b200.dist import count_sharded
+        count_sharded(prog, n, stream=stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_count = int(count_sharded(prog, n, stream=stream).item()) & ((1 << 64) - 1)
+        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_value = valuations / te.item()
+        assert e2e_count == final
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
 
     cpu = None
     if not args.no_cpu_baseline and world == 1:
