@@ -157,6 +157,14 @@ int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
  * caller sums with one all-reduce.  Synchronous on `stream`. */
 int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, void* stream);
 
+/* The plan bfa_count_shard follows (host only, no device needed): the number
+ * of pieces, and for the first `capacity` of them the owning rank, the
+ * piece's number of free variables (it covers 2^piece_vars valuations) and
+ * its estimated work (0 = proved identically 0 by the Reduction).  Every
+ * rank computes the same plan. */
+int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_vars, uint64_t* work, int capacity,
+                   int* n_pieces);
+
 /* The slice [mu_lo, mu_hi) of the DNF vector, asynchronously on `stream`:
  * bit (mu - mu_lo) at word (mu - mu_lo) >> 6 of out_dev (device,
  * ceil((mu_hi-mu_lo)/64) words).  mu_lo, mu_hi multiples of 64, or the whole

@@ -51,6 +51,8 @@ _SIGS = {
     "bfa_batch_count": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int), _c.c_void_p, _c.c_void_p]),
     "bfa_batch_free": (None, [_c.c_void_p]),
     "bfa_count_shard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
+    "bfa_shard_plan": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
+                                  _c.POINTER(_c.c_uint64), _c.c_int, _c.POINTER(_c.c_int)]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -181,6 +183,16 @@ class Program:
         out = _u64_out(out, 1)
         _check(_load().bfa_count_shard(self._h, n, rank, world, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
         return out
+
+    def shard_plan(self, n: int, world: int):
+        """bfa_shard_plan (host only): [(owner rank, free variables, work)] per piece."""
+        lib = _load()
+        np_ = ctypes.c_int()
+        _check(lib.bfa_shard_plan(self._h, n, world, None, None, None, 0, ctypes.byref(np_)))
+        k = np_.value
+        own, nv, wk = (ctypes.c_int * k)(), (ctypes.c_int * k)(), (ctypes.c_uint64 * k)()
+        _check(lib.bfa_shard_plan(self._h, n, world, own, nv, wk, k, ctypes.byref(np_)))
+        return [(own[i], nv[i], wk[i]) for i in range(k)]
 
     def eval(self, n: int, out=None):
         """bfa_eval: the full-DNF vector as words_for(n) device int64 words (synchronous)."""

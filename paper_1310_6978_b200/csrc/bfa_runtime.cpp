@@ -712,26 +712,18 @@ int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* c
 int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
                      uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out,
                      uint64_t cap);
-
-// Multi-launch counts (decomposition / kernel cofactoring) replay as a CUDA
-// graph: the first call runs directly (and prepares every kernel), the second
-// captures the launch sequence on an internal non-blocking stream, later
-// calls launch the instantiated graph on the caller's stream.
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0) {
-  const bool multi = p && (p->opt.split_pieces > 1 || p->opt.kernel_cofactor_bits > 0);
-  if (!multi || !p->opt.graphs || eval || mu_out || force_roles_k >= 0 || !count_dev)
-    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0);
+
+// Multi-launch counts replay as a CUDA graph: the first call of a key runs
+// directly (and prepares every kernel), the second captures the launch
+// sequence on an internal non-blocking stream (the legacy stream cannot be
+// captured), later calls launch the instantiated graph on the caller's
+// stream.  `body(stream)` issues the work; the key covers everything the
+// recorded launches depend on (program state, options, range, output).
+template <class F>
+int with_graph(const bfa_prog* p, const std::string& key, cudaStream_t st, F body) {
   bfa_prog* mp = const_cast<bfa_prog*>(p);
-  int dev = 0;
-  cudaGetDevice(&dev);
-  const Options& o = p->opt;
-  std::ostringstream k;
-  k << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << "|" << o.slot_bits << ','
-    << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic << ',' << o.engine << ','
-    << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search << ',' << o.role_budget
-    << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ',' << o.split_pieces;
-  const std::string key = k.str();
   int calls;
   cudaGraphExec_t exec = nullptr;
   {
@@ -747,14 +739,13 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     g_launches += mp->graph_launches[key];
     return BFA_OK;
   }
-  if (calls == 0)
-    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
-  // capture on an internal stream ordered after the caller's stream
+  if (calls == 0) return body(st);
+  int dev = 0;
+  cudaGetDevice(&dev);
   static thread_local std::map<int, cudaStream_t> cap_streams;
   cudaStream_t cs = cap_streams[dev];
   if (!cs) {
-    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
-      return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return body(st);
     cap_streams[dev] = cs;
   }
   cudaGraph_t graph = nullptr;
@@ -762,7 +753,7 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
   int rc = BFA_OK;
   if (e == cudaSuccess) {
-    rc = run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, cs, eval, force_roles_k, mu_out, cap);
+    rc = body(cs);
     e = cudaStreamEndCapture(cs, &graph);
   }
   const uint64_t captured = g_launches - l0;
@@ -772,7 +763,7 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
     if (graph) cudaGraphDestroy(graph);
     std::lock_guard<std::mutex> lk(mp->mu);
     mp->opt.graphs = 0;  // not capturable here: run directly from now on
-    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+    return body(st);
   }
   e = cudaGraphInstantiate(&exec, graph, 0);
   cudaGraphDestroy(graph);
@@ -786,6 +777,30 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaGraphLaunch: %s", cudaGetErrorString(e));
   g_launches += captured;
   return BFA_OK;
+}
+
+std::string options_key(const Options& o) {
+  std::ostringstream k;
+  k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
+    << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
+    << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
+    << o.split_pieces;
+  return k.str();
+}
+
+int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
+              cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out, uint64_t cap) {
+  const bool multi = p && (p->opt.split_pieces > 1 || p->opt.kernel_cofactor_bits > 0);
+  if (!multi || !p->opt.graphs || eval || mu_out || force_roles_k >= 0 || !count_dev)
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::ostringstream k;
+  k << "range|" << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << '|'
+    << options_key(p->opt);
+  return with_graph(p, k.str(), st, [&](cudaStream_t s) {
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, s, eval, force_roles_k, mu_out, cap);
+  });
 }
 
 int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
@@ -961,6 +976,51 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
 int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
                  int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out);
 
+// The sharding plan (host only, deterministic): pieces of the cube and the
+// rank owning each (LPT on the estimated work).
+struct ShardPlan {
+  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
+  std::vector<int> owner;
+  std::vector<uint64_t> load;
+  std::vector<uint64_t> work;
+};
+
+int shard_plan(const bfa_prog* p, int n, int world, ShardPlan* plan) {
+  if (world < 1) return set_err(BFA_E_ARG, "world %d", world);
+  if (n < 0 || n > 63 || p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "bad n=%d", n);
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  const std::string key = "shard." + std::to_string(n) + "." + std::to_string(world) + "." + options_key(p->opt);
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it != mp->cofactors.end()) plan->kids = &it->second;
+  }
+  if (!plan->kids) {
+    std::vector<std::unique_ptr<bfa_prog>> made =
+        decompose(p, bfa::assume(p->parsed, n, 0, 0, nullptr), n, std::max(4 * world, p->opt.split_pieces));
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
+    plan->kids = &it->second;
+  }
+  auto& kids = *plan->kids;
+  std::vector<std::pair<uint64_t, size_t>> work;
+  plan->work.assign(kids.size(), 0);
+  for (size_t i = 0; i < kids.size(); i++) {
+    plan->work[i] = piece_work(kids[i].get(), kids[i]->piece_nv);
+    work.push_back({plan->work[i], i});
+  }
+  std::stable_sort(work.begin(), work.end(), [](auto& x, auto& y) { return x.first > y.first; });
+  plan->load.assign(world, 0);
+  plan->owner.assign(kids.size(), 0);
+  for (auto& wi : work) {
+    int r = (int)(std::min_element(plan->load.begin(), plan->load.end()) - plan->load.begin());
+    plan->owner[wi.second] = r;
+    plan->load[r] += wi.first;
+  }
+  return BFA_OK;
+}
+
 int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, cudaStream_t st,
                 std::string* report) {
   if (world < 1 || rank < 0 || rank >= world) return set_err(BFA_E_ARG, "rank %d of %d", rank, world);
@@ -969,47 +1029,29 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
     if (rank != 0) return cudaMemsetAsync(count_dev, 0, 8, st) == cudaSuccess ? BFA_OK : set_err(BFA_E_CUDA, "memset");
     return run_range(p, n, 0, n == 63 ? (1ull << 63) : (1ull << n), nullptr, count_dev, st, false);
   }
-  bfa_prog* mp = const_cast<bfa_prog*>(p);
-  const std::string key = "shard." + std::to_string(n) + "." + std::to_string(world);
-  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(mp->mu);
-    auto it = mp->cofactors.find(key);
-    if (it != mp->cofactors.end()) kids = &it->second;
-  }
-  if (!kids) {
-    std::vector<std::unique_ptr<bfa_prog>> made =
-        decompose(p, bfa::assume(p->parsed, n, 0, 0, nullptr), n, std::max(4 * world, p->opt.split_pieces));
-    std::lock_guard<std::mutex> lk(mp->mu);
-    auto it = mp->cofactors.find(key);
-    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
-    kids = &it->second;
-  }
-  // LPT assignment (identical on every rank)
-  std::vector<std::pair<uint64_t, size_t>> work;
-  for (size_t i = 0; i < kids->size(); i++)
-    work.push_back({piece_work((*kids)[i].get(), (*kids)[i]->piece_nv), i});
-  std::stable_sort(work.begin(), work.end(), [](auto& a, auto& b) { return a.first > b.first; });
-  std::vector<uint64_t> load(world, 0);
-  std::vector<int> owner(kids->size(), 0);
-  for (auto& wi : work) {
-    int r = (int)(std::min_element(load.begin(), load.end()) - load.begin());
-    owner[wi.second] = r;
-    load[r] += wi.first;
-  }
+  ShardPlan plan;
+  int rc = shard_plan(p, n, world, &plan);
+  if (rc) return rc;
   int dev;
   DevInfo di;
-  int rc = current_device(&dev, &di);
-  if (rc) return rc;
+  if ((rc = current_device(&dev, &di))) return rc;
   int kernels = 0;
-  if ((rc = count_pieces(*kids, owner, rank, dev, di.sms, count_dev, st, &kernels))) return rc;
+  auto body = [&](cudaStream_t s) { return count_pieces(*plan.kids, plan.owner, rank, dev, di.sms, count_dev, s, &kernels); };
+  if (p->opt.graphs) {
+    std::ostringstream k;
+    k << "shard|" << dev << '.' << n << '.' << rank << '.' << world << '.' << (uintptr_t)count_dev << '|'
+      << options_key(p->opt);
+    rc = with_graph(p, k.str(), st, body);
+  } else {
+    rc = body(st);
+  }
+  if (rc) return rc;
   if (report) {
     std::ostringstream js;
-    js << "{\"variant\": \"cofactor-sharded\", \"pieces\": " << kids->size() << ", \"valuations_decided\": "
+    js << "{\"variant\": \"cofactor-sharded\", \"pieces\": " << plan.kids->size() << ", \"valuations_decided\": "
        << g_decided << ", \"cells_lop3\": " << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad
-       << ", \"rank\": " << rank
-       << ", \"world\": " << world << ", \"kernels\": " << kernels << ", \"load\": [";
-    for (int r = 0; r < world; r++) js << (r ? ", " : "") << load[r];
+       << ", \"rank\": " << rank << ", \"world\": " << world << ", \"pieces_launched\": " << kernels << ", \"load\": [";
+    for (int r = 0; r < world; r++) js << (r ? ", " : "") << plan.load[r];
     js << "]}";
     *report = js.str();
   }
@@ -1169,6 +1211,22 @@ int bfa_compile(const char* expr, bfa_prog** out) {
   if (bfa::parse_program(expr, &p->parsed, &err) != 0) return set_err(BFA_E_PARSE, "%s", err.c_str());
   fill_info(p.get());
   *out = p.release();
+  return BFA_OK;
+}
+
+int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_vars, uint64_t* work, int capacity,
+                   int* n_pieces) {
+  if (!p || !n_pieces) return set_err(BFA_E_ARG, "NULL argument");
+  ShardPlan plan;
+  int rc = shard_plan(p, n, world, &plan);
+  if (rc) return rc;
+  const int np = (int)plan.kids->size();
+  *n_pieces = np;
+  for (int i = 0; i < std::min(np, capacity); i++) {
+    if (owner) owner[i] = plan.owner[i];
+    if (piece_vars) piece_vars[i] = (*plan.kids)[i]->piece_nv;
+    if (work) work[i] = plan.work[i];
+  }
   return BFA_OK;
 }
 

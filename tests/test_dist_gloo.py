@@ -70,3 +70,47 @@ def test_rank_range_rules():
         rank_range(7, 0, 8)
     with pytest.raises(ValueError):
         rank_range(36, 8, 8)
+
+
+def _plan_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1310_6978_b200 as bfa
+    import workloads as W
+    out = []
+    for cfg in ("c4", "c5"):
+        text, n, _ = W.config(cfg)
+        plan = bfa.Program(text).shard_plan(n, world)      # host only: no GPU, no communication
+        flat = torch.tensor([x for piece in plan for x in piece], dtype=torch.int64)
+        gathered = [torch.zeros_like(flat) for _ in range(world)]
+        dist.all_gather(gathered, flat)
+        out.append((cfg, n, plan, all(torch.equal(g, flat) for g in gathered)))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_shard_plan_identical_on_all_ranks(world):
+    """Work-balanced cofactor sharding (bfa_count_shard) needs no exchange to
+    agree on who counts what: every rank derives the same plan on its own.
+    The pieces tile the 2^n cube, each non-constant piece has one owner, and
+    the estimated loads are balanced."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_plan_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, out in res:
+        for cfg, n, plan, same in out:
+            assert same, cfg
+            assert sum(1 << nv for _, nv, _ in plan) == 1 << n
+            assert {o for o, _, w in plan if w} == set(range(world))
+            load = [sum(w for o, _, w in plan if o == r) for r in range(world)]
+            assert max(load) <= 1.5 * sum(load) / world

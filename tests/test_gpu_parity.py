@@ -323,8 +323,10 @@ def test_count_shard_sums_to_count():
         full = bfa.Program(text).count(n)
         p = bfa.Program(text)
         for world in (2, 4, 8):
-            shares = [int(p.count_shard(n, r, world).item()) for r in range(world)]
-            assert sum(shares) == full, (cfg, world, shares)
+            out = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+            for rep in range(3):          # direct, graph capture, graph replay
+                shares = [int(p.count_shard(n, r, world, out=out[r]).item()) for r in range(world)]
+                assert sum(shares) == full, (cfg, world, rep, shares)
             load = bfa.last_launch()["load"]
             assert len(load) == world and max(load) <= 1.6 * sum(load) / world, (cfg, world, load)
 
