@@ -161,7 +161,7 @@ def run_reference(args):
     value = statistics.median(steps)
     line = {"impl": "reference", "metric": "valuations/s", "value": value, "unit": "valuations/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": (1 << n) / value * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": (1 << n) / value * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bool (C int per valuation)", "data": "synthetic",
             "config": config_block(args.config, n, None, 1),
             "cpu_baseline": {"value": value, "unit": "valuations/s", "cores": cores, "kind": "oracle",

@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdarg>
@@ -212,6 +215,66 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   return BFA_OK;
 }
 
+// ------------------------------------------------------------ persistent cache
+// Cubins and role-search results are cached on disk (keyed by a hash of the
+// generated source / of the program DAG and variant) so later processes
+// (other ranks, the next bench run) skip NVRTC and the search.  Only
+// preparation time depends on it, never results.  $BFA_JIT_CACHE=0 disables.
+uint64_t fnv64(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* c = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; i++) { h ^= c[i]; h *= 1099511628211ull; }
+  return h;
+}
+
+const std::string& cache_dir() {
+  static std::string dir = [] {
+    const char* env = getenv("BFA_JIT_CACHE");
+    if (env && std::string(env) == "0") return std::string();
+    std::string d = env && *env ? env : std::string(getenv("HOME") ? getenv("HOME") : "/tmp") + "/.cache/bfa_jit";
+    for (size_t i = 1; i <= d.size(); i++)
+      if (i == d.size() || d[i] == '/') mkdir(d.substr(0, i).c_str(), 0755);
+    return d;
+  }();
+  return dir;
+}
+
+bool cache_read(const std::string& name, std::vector<char>* out) {
+  if (cache_dir().empty()) return false;
+  FILE* f = fopen((cache_dir() + "/" + name).c_str(), "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  long sz = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out->resize(sz > 0 ? (size_t)sz : 0);
+  bool ok = sz > 0 && fread(out->data(), 1, (size_t)sz, f) == (size_t)sz;
+  fclose(f);
+  return ok;
+}
+
+void cache_write(const std::string& name, const void* data, size_t n) {
+  if (cache_dir().empty()) return;
+  char tmp[64];
+  snprintf(tmp, sizeof tmp, ".tmp.%d.%llx", (int)getpid(), (unsigned long long)fnv64(data, n));
+  std::string t = cache_dir() + "/" + name + tmp;
+  FILE* f = fopen(t.c_str(), "wb");
+  if (!f) return;
+  bool ok = fwrite(data, 1, n, f) == n;
+  fclose(f);
+  if (ok) rename(t.c_str(), (cache_dir() + "/" + name).c_str());
+  else remove(t.c_str());
+}
+
+int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin) {
+  char name[64];
+  static const char salt[] = "bfa-cubin-v1|sm_100a|nvrtc-12.9|";
+  snprintf(name, sizeof name, "k_%016llx.cubin",
+           (unsigned long long)fnv64(src.data(), src.size(), fnv64(salt, sizeof salt)));
+  if (cache_read(name, cubin)) return BFA_OK;
+  int rc = nvrtc_compile(src, cubin);
+  if (rc == BFA_OK) cache_write(name, cubin->data(), cubin->size());
+  return rc;
+}
+
 // ------------------------------------------------------------ options
 struct Options {
   int slot_bits = 2;
@@ -289,7 +352,25 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     auto it = p->roles.find(key);
     if (it != p->roles.end()) { spec->perm = it->second; return; }
   }
-  std::vector<int8_t> perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull);
+  // persistent cache: hash of the DAG reachable from the root + the variant
+  static const char salt[] = "bfa-roles-v1|";
+  uint64_t h = fnv64(key.data(), key.size(), fnv64(salt, sizeof salt));
+  for (const bfa::Node& nd : p->parsed.dag.nodes) {
+    uint32_t rec[4] = {(uint32_t)nd.kind | ((uint32_t)nd.tt << 8), nd.a, nd.b, nd.val};
+    h = fnv64(rec, sizeof rec, h);
+  }
+  h = fnv64(&p->parsed.root, sizeof p->parsed.root, h);
+  char name[64];
+  snprintf(name, sizeof name, "r_%016llx.perm", (unsigned long long)h);
+  std::vector<char> buf;
+  std::vector<int8_t> perm;
+  if (cache_read(name, &buf) && (buf.size() == 64 || buf.size() == 1)) {
+    if (buf.size() == 64) perm.assign(buf.begin(), buf.end());
+  } else {
+    perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull);
+    if (perm.empty()) { char z = 0; cache_write(name, &z, 1); }
+    else cache_write(name, perm.data(), perm.size());
+  }
   std::lock_guard<std::mutex> lk(p->mu);
   p->roles[key] = perm;
   spec->perm = perm;
@@ -317,7 +398,7 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
     ne->source = bfa::emit_kernel(p->parsed, spec, &ne->stats);
-    int rc = nvrtc_compile(ne->source, &ne->cubin);
+    int rc = nvrtc_compile_cached(ne->source, &ne->cubin);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->jit.find(key);
@@ -359,7 +440,7 @@ int get_kernel_src(const bfa_prog* cp, const std::string& key, const std::string
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
     ne->source = src;
-    int rc = nvrtc_compile(ne->source, &ne->cubin);
+    int rc = nvrtc_compile_cached(ne->source, &ne->cubin);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->jit.find(key);
@@ -1471,14 +1552,15 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     else if (est <= 2000.0) { thi = hi; tlo = hi - (1ull << k_free); }
     int best_j = 0, best_sp = 0;
     float best_ms = 1e30f;
-    std::vector<std::pair<int, int>> trials = {{0, 0}, {0, 2}, {0, 4}, {0, 6}, {8, -1}, {16, -2}};
-    for (auto tr : trials) {
-      int sp = tr.first, jj = tr.second;
-      if (jj < 0) jj = std::max(0, best_j + jj + 1);  // relative to the best j so far
-      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj + (sp ? 4 : 0)) continue;
+    auto trial = [&](int sp, int jj) -> int {
+      if (jj < 0 || jj > 8) return BFA_OK;
+      for (auto& done : kcof)
+        if (done.first == jj + 100 * sp) return BFA_OK;
+      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj + (sp ? 4 : 0)) return BFA_OK;
       p->opt.kernel_cofactor_bits = jj;
       p->opt.split_pieces = sp;
-      if ((rc = run_range(p, n, tlo, thi, nullptr, d, st, false))) { p->opt = cands[best].o; break; }
+      int r2 = run_range(p, n, tlo, thi, nullptr, d, st, false);
+      if (r2) return r2;
       float bm = 1e30f;
       for (int r = 0; r < 2; r++) {
         cudaEventRecord(e0, st);
@@ -1491,7 +1573,23 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
       }
       kcof.push_back({jj + 100 * sp, bm});
       if (bm < best_ms) { best_ms = bm; best_j = jj; best_sp = sp; }
+      return BFA_OK;
+    };
+    // stage A: cofactor bits without pieces; B: Shannon pieces at ~ the same
+    // total split depth; C: refine around the best
+    for (int jj : {0, 2, 4, 6})
+      if ((rc = trial(0, jj))) break;
+    const int ja = best_j;
+    if (!rc && ja > 0) {
+      for (auto tr : {std::make_pair(16, ja - 1), std::make_pair(64, ja - 2)})
+        if ((rc = trial(tr.first, tr.second))) break;
+      if (!rc && best_sp > 0) {
+        const int sp = best_sp, jb = best_j;
+        for (auto tr : {std::make_pair(sp, jb + 1), std::make_pair(sp * 2, jb)})
+          if ((rc = trial(tr.first, tr.second))) break;
+      }
     }
+    if (rc) p->opt = cands[best].o;
     p->opt.kernel_cofactor_bits = best_j;
     p->opt.split_pieces = best_sp;
   }
@@ -1531,7 +1629,7 @@ int bfa_batch_create(const bfa_prog* const* progs, int count, bfa_batch** out) {
     ps.push_back(&progs[i]->parsed);
   }
   b->source = bfa::emit_batch(ps, 8);
-  int rc = nvrtc_compile(b->source, &b->cubin);
+  int rc = nvrtc_compile_cached(b->source, &b->cubin);
   if (rc) return rc;
   *out = reinterpret_cast<bfa_batch*>(b.release());
   return BFA_OK;
