@@ -113,6 +113,14 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   HBM slot arrays
  *   "segment_remat" recompute shared cells whose cone has <= this many cells in
  *                   each segment instead of storing them (default 2)
+ *   "kernel_cofactor_bits" count: split aligned sub-cubes into 2^j cofactor
+ *                   programs, one kernel each (default 0; autotune sets it)
+ *   "split_pieces"  count: Shannon-decompose aligned sub-cubes into this many
+ *                   non-constant pieces first (default 0; autotune sets it)
+ *   "graphs"        replay multi-launch counts as CUDA graphs (default 1)
+ *   "streams"       side streams for independent pieces / cofactors (default 4)
+ *   "multi_body"    1: a split's cofactor children as one multi-body launch
+ *                   (default 0)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 

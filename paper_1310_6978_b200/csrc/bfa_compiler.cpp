@@ -951,7 +951,9 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   std::ostringstream os;
   os << "// generated by libbfa: " << (spec.mode == KM_COUNT ? "count" : "eval")
      << (spec.generic ? " generic" : " specialised") << " s=" << spec.slot_bits << " t=" << spec.thread_bits
-     << " m=" << spec.inner_bits << (spec.perm.empty() ? "" : " (permuted roles)") << "\n" << kPrelude;
+     << " m=" << spec.inner_bits << (spec.perm.empty() ? "" : " (permuted roles)") << "\n";
+  const bool as_body = !spec.body_name.empty() && !spec.generic;
+  if (!as_body) os << kPrelude;
   Built b;
   build_specialised(prog, spec, &b);
   Dag& D = b.D;
@@ -1048,11 +1050,17 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     for (int v = 0; v < 64; v++) st.inner_vars += used[v];
   } else {
     const int unit = s + t + m;
-    os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
-       << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
-       << enum_params << ") {\n"
-       << "  const u32 tid = threadIdx.x;\n"
-       << "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n"
+    if (as_body)
+      os << "__device__ __noinline__ void " << spec.body_name
+         << "(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
+         << enum_params << ", const u32 bid_, const u32 nb_) {\n";
+    else
+      os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
+         << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
+         << enum_params << ") {\n";
+    os << "  const u32 tid = threadIdx.x;\n"
+       << (as_body ? "  const u64 q = o_count / nb_, rr = o_count % nb_, b = bid_;\n"
+                   : "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n")
        << "  const u64 o_begin = b * q + (b < rr ? b : rr);\n"
        << "  const u64 o_end = o_begin + q + (b < rr ? 1ull : 0ull);\n";
     for (int v = 0; v < 64; v++)
@@ -1248,6 +1256,32 @@ SegPlan emit_segmented(const Parsed& prog, KernelMode mode, bool fuse_count, int
     plan.emitted += E.cells_emitted;
   }
   return plan;
+}
+
+std::string emit_multi(const std::vector<const Parsed*>& progs, const std::vector<KernelSpec>& specs,
+                       std::vector<KernelStats>* stats) {
+  std::ostringstream os;
+  os << "// generated by libbfa: multi-body kernel of " << progs.size() << " programs\n" << kPrelude;
+  if (stats) stats->assign(progs.size(), KernelStats());
+  for (size_t c = 0; c < progs.size(); c++) {
+    KernelSpec sp = specs[c];
+    sp.body_name = "bfa_body_" + std::to_string(c);
+    KernelStats st;
+    os << emit_kernel(*progs[c], sp, &st);
+    if (stats) (*stats)[c] = st;
+  }
+  const KernelSpec& s0 = specs[0];
+  const std::string bounds = std::to_string(1 << s0.thread_bits) +
+                             (s0.min_blocks > 0 ? ", " + std::to_string(s0.min_blocks) : "");
+  os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
+     << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, "
+     << "u64* __restrict__ count, const u32 bpc) {\n"
+     << "  const u32 c = blockIdx.x / bpc, bid = blockIdx.x - c * bpc;\n"
+     << "  switch (c) {\n";
+  for (size_t c = 0; c < progs.size(); c++)
+    os << "    case " << c << ": bfa_body_" << c << "(A, o_count, out_base_w, out, count, bid, bpc); break;\n";
+  os << "  }\n}\n";
+  return os.str();
 }
 
 std::string emit_batch(const std::vector<const Parsed*>& progs, int thread_bits) {

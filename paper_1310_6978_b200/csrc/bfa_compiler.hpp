@@ -136,6 +136,8 @@ struct KernelSpec {
   int min_blocks = 0;         // >0: __launch_bounds__ minimum resident blocks per SM
   std::vector<int8_t> perm;   // count mode: bit position of each variable in the
                               // word/valuation index (empty = identity)
+  std::string body_name;      // non-empty: emit the specialised kernel as a
+                              // __device__ __noinline__ body of a multi-body kernel
 };
 
 struct KernelStats {
@@ -146,6 +148,13 @@ struct KernelStats {
   uint32_t inner_vars = 0, outer_vars = 0, thread_vars = 0;
   uint32_t words_per_iter = 1;
 };
+
+// One kernel for several programs (kernel-level cofactor children of one
+// piece): each child's specialised kernel becomes a noinline device body;
+// block b runs body b / bpc with block index b % bpc of bpc blocks.  Kernel
+// signature: (u64 A, u64 o_count, u64 out_base_w, u32* out, u64* count, u32 bpc).
+std::string emit_multi(const std::vector<const Parsed*>& progs, const std::vector<KernelSpec>& specs,
+                       std::vector<KernelStats>* stats);
 
 // Modelled time per thread-iteration of the variant's best cover.
 double model_cost(const Parsed& prog, const KernelSpec& spec);

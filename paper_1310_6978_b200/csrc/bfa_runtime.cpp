@@ -56,8 +56,10 @@ thread_local bool g_forked = false;
 // Fork/join of independent launches over side streams (their counts only
 // meet in atomics), so short kernels overlap instead of idling SMs during
 // each other's tails; capturable into a CUDA graph as parallel branches.
+thread_local int g_fork_width = 4;  // side streams per fork (option "streams")
+
 struct Fork {
-  static constexpr int K = 4;
+  static constexpr int K = 16;       // pool size; a fork uses g_fork_width of them
   cudaStream_t base = nullptr;
   bool active = false;
   int next = 0;
@@ -77,15 +79,18 @@ struct Fork {
     if (g_forked) return;
     pl = &pool(dev);
     if (!pl->ok) return;
+    width = std::max(1, std::min(K, g_fork_width));
+    if (width == 1) return;
     if (cudaEventRecord(pl->ev[K], st) != cudaSuccess) return;
-    for (int i = 0; i < K; i++) cudaStreamWaitEvent(pl->s[i], pl->ev[K], 0);
+    for (int i = 0; i < width; i++) cudaStreamWaitEvent(pl->s[i], pl->ev[K], 0);
     active = true;
     g_forked = true;
   }
-  cudaStream_t stream() { return active ? pl->s[next++ % K] : base; }
+  int width = 1;
+  cudaStream_t stream() { return active ? pl->s[next++ % width] : base; }
   void join() {
     if (!active) return;
-    for (int i = 0; i < K; i++) {
+    for (int i = 0; i < width; i++) {
       cudaEventRecord(pl->ev[i], pl->s[i]);
       cudaStreamWaitEvent(base, pl->ev[i], 0);
     }
@@ -293,6 +298,8 @@ struct Options {
   int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
   int split_pieces = 0;          // count: Shannon-decompose aligned sub-cubes into this many pieces first
   int graphs = 1;                // replay multi-launch counts as CUDA graphs
+  int streams = 4;               // side streams for independent pieces / cofactors
+  int multi_body = 0;            // 1: cofactor children of a piece as ONE multi-body launch (measured slower: occupancy of the largest child)
 };
 
 struct JitEntry {
@@ -320,6 +327,14 @@ struct bfa_prog {
   // CUDA graphs of multi-launch counts: key -> (calls seen, instantiated graph)
   std::map<std::string, std::pair<int, cudaGraphExec_t>> graphs;
   std::map<std::string, uint64_t> graph_launches;  // kernels per replay
+  // multi-body kernels of cofactor children: key -> (source key, per-child stats, plan)
+  struct Multi {
+    std::string src_key, source;
+    std::vector<bfa::KernelStats> stats;
+    int m = 0;
+    uint64_t O = 0;
+  };
+  std::map<std::string, Multi> multis;
   ~bfa_prog() {
     for (auto& g : graphs)
       if (g.second.second) cudaGraphExecDestroy(g.second.second);
@@ -865,12 +880,13 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body;
   return k.str();
 }
 
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
               cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out, uint64_t cap) {
+  if (p && !g_forked) g_fork_width = p->opt.streams;
   const bool multi = p && (p->opt.split_pieces > 1 || p->opt.kernel_cofactor_bits > 0);
   if (!multi || !p->opt.graphs || eval || mu_out || force_roles_k >= 0 || !count_dev)
     return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
@@ -882,6 +898,147 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   return with_graph(p, k.str(), st, [&](cudaStream_t s) {
     return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, s, eval, force_roles_k, mu_out, cap);
   });
+}
+
+// The kernel-level cofactor split of an aligned 2^k sub-cube (host only,
+// cached in the program): 2^j children over k - j variables.  Children are
+// compiled here unless they will run as one multi-body kernel.
+std::vector<std::unique_ptr<bfa_prog>>* ensure_split(const bfa_prog* p, int n, uint64_t mu_lo, int k, int j, int sms,
+                                                     std::string* key_out, int* rc_out) {
+  *rc_out = BFA_OK;
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
+  const uint64_t top_vals = mu_lo & top_mask;
+  const std::string key = std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) + "." +
+                          std::to_string(j);
+  *key_out = key;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->cofactors.find(key);
+    if (it != mp->cofactors.end()) return &it->second;
+  }
+  // the range's program over its k free variables, then j cofactor variables
+  bfa::Parsed base = bfa::assume(p->parsed, n, top_mask, top_vals, nullptr);
+  std::vector<int> J = bfa::choose_cofactor_vars(base, k, j);
+  uint64_t jmask = 0;
+  for (int v : J) jmask |= 1ull << v;
+  std::vector<std::unique_ptr<bfa_prog>> made;
+  for (uint64_t c = 0; c < (1ull << J.size()); c++) {
+    uint64_t vals = 0;
+    for (size_t b = 0; b < J.size(); b++) vals |= ((c >> b) & 1) << J[b];
+    auto q = std::make_unique<bfa_prog>();
+    q->parsed = bfa::assume(base, k, jmask, vals, nullptr);
+    q->opt = p->opt;
+    q->opt.kernel_cofactor_bits = 0;
+    q->opt.split_pieces = 0;
+    q->opt.graphs = 0;
+    fill_info(q.get());
+    made.push_back(std::move(q));
+  }
+  const int kk = k - (int)J.size();
+  if (!p->opt.multi_body) {  // compile every child's kernel in parallel (host only)
+    std::vector<std::thread> th;
+    std::vector<int> rcs(made.size(), 0);
+    for (size_t i = 0; i < made.size(); i++)
+      th.emplace_back([&, i] { rcs[i] = prepare_count(made[i].get(), kk, sms); });
+    for (auto& t : th) t.join();
+    for (int r : rcs)
+      if (r) { *rc_out = r; return nullptr; }
+  }
+  std::lock_guard<std::mutex> lk(mp->mu);
+  auto it = mp->cofactors.find(key);
+  if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
+  return &it->second;
+}
+
+// All non-constant cofactor children of one split as ONE multi-body launch:
+// child c is a noinline device body run by blocks [c * bpc, (c+1) * bpc).
+// Returns BFA_E_ARG (nothing launched) when not applicable: fewer than two
+// non-constant children, or children whose whole-cube plan is not a single
+// specialised segment.
+int ensure_multi(bfa_prog* mp, const std::string& kkey, std::vector<std::unique_ptr<bfa_prog>>& kids, int kk,
+                 int sms, bfa_prog::Multi** out, std::vector<size_t>* live_out) {
+  std::vector<size_t> live;
+  for (size_t i = 0; i < kids.size(); i++)
+    if (kids[i]->info.const_value != 0) live.push_back(i);
+  if (live_out) *live_out = live;
+  if (live.size() < 2 || kk < 5 || kids[live[0]]->opt.force_generic || kids[live[0]]->opt.engine ||
+      kids[live[0]]->info.luts > 8000)
+    return set_err(BFA_E_ARG, "multi-body not applicable");
+  for (size_t i : live)
+    if (kids[i]->info.luts > 8000) return set_err(BFA_E_ARG, "multi-body not applicable");
+  const Options& o = kids[live[0]]->opt;
+  const int T = 1 << o.thread_bits;
+  const DevInfo di{sms};
+  const std::string mkey = "mb|" + kkey + "|" + options_key(o);
+  bfa_prog::Multi* mu = nullptr;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    auto it = mp->multis.find(mkey);
+    if (it != mp->multis.end()) mu = &it->second;
+  }
+  if (!mu) {
+    const int full_grid = di.sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
+    std::vector<Segment> segs = plan(o, o.slot_bits, kk, 0, 1ull << (kk - 5), full_grid);
+    if (segs.size() != 1 || segs[0].generic) return set_err(BFA_E_ARG, "multi-body not applicable");
+    bfa::KernelSpec base;
+    base.mode = bfa::KM_COUNT; base.generic = false; base.slot_bits = o.slot_bits; base.thread_bits = o.thread_bits;
+    base.inner_bits = segs[0].m; base.dual_pipe = o.dual_pipe; base.imad_cost_pct = o.imad_cost_pct;
+    base.min_blocks = o.min_blocks;
+    std::vector<bfa::KernelSpec> specs(live.size(), base);
+    {  // role searches in parallel (cached per child and on disk)
+      std::vector<std::thread> th;
+      for (size_t c = 0; c < live.size(); c++)
+        th.emplace_back([&, c] { resolve_roles(kids[live[c]].get(), &specs[c], kk); });
+      for (auto& t : th) t.join();
+    }
+    bfa_prog::Multi m;
+    std::vector<const bfa::Parsed*> progs;
+    for (size_t i : live) progs.push_back(&kids[i]->parsed);
+    m.source = bfa::emit_multi(progs, specs, &m.stats);
+    m.src_key = mkey;
+    m.m = segs[0].m;
+    m.O = (1ull << (kk - 5)) >> (o.slot_bits + o.thread_bits + segs[0].m);
+    std::lock_guard<std::mutex> lk(mp->mu);
+    mu = &mp->multis.emplace(mkey, std::move(m)).first->second;
+  }
+  int rc = get_kernel_src(mp, mu->src_key, mu->source, o.thread_bits, -1, nullptr, nullptr);  // NVRTC (cached)
+  if (rc) return rc;
+  *out = mu;
+  return BFA_OK;
+}
+
+int multi_body_count(bfa_prog* mp, const std::string& kkey, std::vector<std::unique_ptr<bfa_prog>>& kids, int kk,
+                     int dev, const DevInfo& di, uint64_t* count_dev, cudaStream_t st, int* kernels, int* zero,
+                     int* one, double* l3, double* im) {
+  for (auto& q : kids) {
+    if (q->info.const_value == 0) (*zero)++;
+    if (q->info.const_value == 1) (*one)++;
+  }
+  bfa_prog::Multi* mu = nullptr;
+  std::vector<size_t> live;
+  int rc = ensure_multi(mp, kkey, kids, kk, di.sms, &mu, &live);
+  if (rc) return rc;
+  const Options& o = kids[live[0]]->opt;
+  const int T = 1 << o.thread_bits;
+  JitEntry* je = nullptr;
+  CUfunction fn;
+  if ((rc = get_kernel_src(mp, mu->src_key, mu->source, o.thread_bits, dev, &je, &fn))) return rc;
+  const int bps = je->occupancy[dev];
+  uint32_t bpc = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(mu->O, (uint64_t)di.sms * bps));
+  uint64_t A = 0, O = mu->O, base_w = 0;
+  uint32_t* out = nullptr;
+  uint64_t* cnt = count_dev;
+  const unsigned grid = (unsigned)(bpc * live.size());
+  void* args[] = {&A, &O, &base_w, &out, &cnt, &bpc};
+  if ((rc = launch(fn, grid, T, st, args))) return rc;
+  *kernels = 1;
+  const double S = 1 << o.slot_bits, it = std::pow(2.0, mu->m), words = (double)(1ull << (kk - 5));
+  for (const auto& stt : mu->stats) {
+    *l3 += words * (stt.luts_inner / S + stt.luts_outer / (S * it));
+    *im += words * ((stt.imads_inner + stt.derived_inner) / S + (stt.imads_outer + stt.derived_outer) / (S * it));
+  }
+  return BFA_OK;
 }
 
 int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
@@ -906,49 +1063,9 @@ int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, u
   int rc = current_device(&dev, &di);
   if (rc) return rc;
   bfa_prog* mp = const_cast<bfa_prog*>(p);
-  const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
-  const uint64_t top_vals = mu_lo & top_mask;
-  const std::string key = std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) + "." +
-                          std::to_string(j);
-  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(mp->mu);
-    auto it = mp->cofactors.find(key);
-    if (it != mp->cofactors.end()) kids = &it->second;
-  }
-  if (!kids) {
-    // the range's program over its k free variables, then j cofactor variables
-    bfa::Parsed base = bfa::assume(p->parsed, n, top_mask, top_vals, nullptr);
-    std::vector<int> J = bfa::choose_cofactor_vars(base, k, j);
-    uint64_t jmask = 0;
-    for (int v : J) jmask |= 1ull << v;
-    std::vector<std::unique_ptr<bfa_prog>> made;
-    for (uint64_t c = 0; c < (1ull << J.size()); c++) {
-      uint64_t vals = 0;
-      for (size_t b = 0; b < J.size(); b++) vals |= ((c >> b) & 1) << J[b];
-      auto q = std::make_unique<bfa_prog>();
-      q->parsed = bfa::assume(base, k, jmask, vals, nullptr);
-      q->opt = p->opt;
-      q->opt.kernel_cofactor_bits = 0;
-      q->opt.split_pieces = 0;
-      q->opt.graphs = 0;
-      fill_info(q.get());
-      made.push_back(std::move(q));
-    }
-    const int kk = k - (int)J.size();
-    {  // compile every child's kernel in parallel (host only)
-      std::vector<std::thread> th;
-      std::vector<int> rcs(made.size(), 0);
-      for (size_t i = 0; i < made.size(); i++)
-        th.emplace_back([&, i] { rcs[i] = prepare_count(made[i].get(), kk, di.sms); });
-      for (auto& t : th) t.join();
-      for (int r : rcs) if (r) return r;
-    }
-    std::lock_guard<std::mutex> lk(mp->mu);
-    auto it = mp->cofactors.find(key);
-    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
-    kids = &it->second;
-  }
+  std::string key;
+  std::vector<std::unique_ptr<bfa_prog>>* kids = ensure_split(p, n, mu_lo, k, j, di.sms, &key, &rc);
+  if (!kids) return rc;
   if (!g_accumulate) {
     cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
     if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
@@ -957,6 +1074,23 @@ int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, u
   int kernels = 0, zero = 0, one = 0;
   std::string first;
   double l3 = 0, im = 0;
+  if (p->opt.multi_body) {
+    rc = multi_body_count(mp, key, *kids, kk, dev, di, count_dev, st, &kernels, &zero, &one, &l3, &im);
+    if (rc != BFA_E_ARG) {  // BFA_E_ARG: not applicable -> separate launches below
+      if (rc) return rc;
+      g_cells_lop3 = l3;
+      g_cells_imad = im;
+      g_decided = (double)zero * (double)(1ull << kk);
+      std::ostringstream js;
+      js << "{\"variant\": \"kernel-cofactored\", \"multi_body\": 1, \"cofactors\": " << kids->size()
+         << ", \"constant_zero\": " << zero << ", \"valuations_decided\": " << g_decided << ", \"constant_one\": " << one
+         << ", \"valuations_per_cofactor\": " << (1ull << kk) << ", \"kernels\": " << kernels << ", \"cells_lop3\": "
+         << l3 << ", \"cells_imad\": " << im << "}";
+      g_last_launch = js.str();
+      return BFA_OK;
+    }
+    zero = one = 0;  // recounted by the separate launches below
+  }
   Fork fork(st, dev);
   for (auto& q : *kids) {
     // a cofactor the Reduction proved identically 0 has no models: decided at
@@ -1053,6 +1187,22 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
   return made;
 }
 
+// Host-side preparation of a piece that splits into cofactor kernels: the
+// split, and its multi-body module (or its children's kernels).
+int prepare_split(const bfa_prog* p, int nv, int sms) {
+  const int j = p->opt.kernel_cofactor_bits;
+  if (nv > 63 || nv < 24 + j || p->info.luts > 8000 || p->opt.segment_cells) return prepare_count(p, nv, sms);
+  std::string key;
+  int rc = BFA_OK;
+  std::vector<std::unique_ptr<bfa_prog>>* kids = ensure_split(p, nv, 0, nv, j, sms, &key, &rc);
+  if (!kids) return rc;
+  if (!p->opt.multi_body) return BFA_OK;
+  const int kk = nv - __builtin_ctzll((unsigned long long)kids->size());
+  bfa_prog::Multi* mu = nullptr;
+  rc = ensure_multi(const_cast<bfa_prog*>(p), key, *kids, kk, sms, &mu, nullptr);
+  return rc == BFA_E_ARG ? BFA_OK : rc;
+}
+
 // Count the pieces owned by `rank` (owner[i] == rank) into count_dev (written).
 int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
                  int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out);
@@ -1113,6 +1263,7 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
   ShardPlan plan;
   int rc = shard_plan(p, n, world, &plan);
   if (rc) return rc;
+  g_fork_width = p->opt.streams;
   int dev;
   DevInfo di;
   if ((rc = current_device(&dev, &di))) return rc;
@@ -1148,8 +1299,11 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
     std::vector<std::thread> th;
     std::vector<int> rcs(kids.size(), 0);
     for (size_t i = 0; i < kids.size(); i++)
-      if (owner[i] == rank && kids[i]->info.const_value != 0 && kids[i]->opt.kernel_cofactor_bits == 0)
-        th.emplace_back([&, i] { rcs[i] = prepare_count(kids[i].get(), kids[i]->piece_nv, sms); });
+      if (owner[i] == rank && kids[i]->info.const_value != 0)
+        th.emplace_back([&, i] {
+          rcs[i] = kids[i]->opt.kernel_cofactor_bits == 0 ? prepare_count(kids[i].get(), kids[i]->piece_nv, sms)
+                                                          : prepare_split(kids[i].get(), kids[i]->piece_nv, sms);
+        });
     for (auto& t : th) t.join();
     for (int r : rcs) if (r) return r;
   }
@@ -1398,6 +1552,8 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }
   else if (k == "split_pieces") { if (v < 0 || v > 1024) return bad(); p->opt.split_pieces = (int)v; }
   else if (k == "graphs") { if (v < 0 || v > 1) return bad(); p->opt.graphs = (int)v; }
+  else if (k == "streams") { if (v < 1 || v > 16) return bad(); p->opt.streams = (int)v; }
+  else if (k == "multi_body") { if (v < 0 || v > 1) return bad(); p->opt.multi_body = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }

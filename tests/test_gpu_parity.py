@@ -274,6 +274,24 @@ def test_kernel_cofactoring():
     assert int(p.count_range(n, lo, lo + (1 << 24)).item()) == oracle.count(text, n, lo, lo + (1 << 24))
 
 
+def test_multi_body_kernels():
+    """Cofactor children fused into one multi-body launch per split give the
+    same counts as separate launches."""
+    for cfg in ("c4", "c5"):
+        text, n, _ = W.config(cfg)
+        full = bfa.Program(text).count(n)
+        p = bfa.Program(text).set_option("kernel_cofactor_bits", 4).set_option("multi_body", 1)
+        assert p.count(n) == full
+        ll = bfa.last_launch()
+        assert ll["constant_zero"] <= ll["cofactors"]
+        if cfg == "c5":                      # C4 keeps a single live child: separate launch
+            assert ll.get("multi_body") == 1
+        p = bfa.Program(text).set_option("split_pieces", 8).set_option("kernel_cofactor_bits", 3)
+        p.set_option("multi_body", 1)
+        for _ in range(3):
+            assert p.count(n) == full
+
+
 def test_split_pieces():
     """Shannon decomposition into pieces (each with kernel-level
     cofactoring) leaves counts unchanged, on the full cube and on an aligned
