@@ -121,6 +121,7 @@ struct Driver {
   CUresult (*GetErrorString)(CUresult, const char**) = nullptr;
   CUresult (*CtxGetCurrent)(CUcontext*) = nullptr;
   CUresult (*CtxGetDevice)(CUdevice*) = nullptr;
+  CUresult (*ModuleUnload)(CUmodule) = nullptr;
   bool ok = false;
   std::string err;
 };
@@ -141,7 +142,8 @@ Driver& drv() {
               get("cuFuncGetAttribute", (void**)&d.FuncGetAttribute) &&
               get("cuGetErrorString", (void**)&d.GetErrorString) &&
               get("cuCtxGetCurrent", (void**)&d.CtxGetCurrent) &&
-              get("cuCtxGetDevice", (void**)&d.CtxGetDevice);
+              get("cuCtxGetDevice", (void**)&d.CtxGetDevice) &&
+              get("cuModuleUnload", (void**)&d.ModuleUnload);
     d.ok = ok;
     if (!ok) d.err = "CUDA driver entry points unavailable (no driver / no device)";
   });
@@ -307,8 +309,13 @@ struct JitEntry {
   std::vector<char> cubin;
   bfa::KernelStats stats;
   std::map<int, CUfunction> fn;   // per device
+  std::map<int, CUmodule> mod;    // per device (unloaded with the entry)
   std::map<int, int> occupancy;   // blocks per SM per device
   int regs = 0;
+  ~JitEntry() {
+    for (auto& m : mod)
+      if (m.second && drv().ModuleUnload) drv().ModuleUnload(m.second);
+  }
 };
 
 }  // namespace
@@ -430,6 +437,7 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
       CUfunction k;
       r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
       if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      e->mod[dev] = mod;
       int nb = 1;
       drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 1 << spec.thread_bits, 0);
       drv().FuncGetAttribute(&e->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
@@ -472,6 +480,7 @@ int get_kernel_src(const bfa_prog* cp, const std::string& key, const std::string
       CUfunction k;
       r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
       if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      e->mod[dev] = mod;
       int nb = 1;
       drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 1 << thread_bits, 0);
       drv().FuncGetAttribute(&e->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);
@@ -1427,9 +1436,14 @@ struct bfa_batch_s {
   std::string source;
   std::vector<char> cubin;
   std::map<int, CUfunction> fn;
+  std::map<int, CUmodule> mod;
   std::map<int, int> occupancy;
   int regs = 0;
   std::mutex mu;
+  ~bfa_batch_s() {
+    for (auto& m : mod)
+      if (m.second && drv().ModuleUnload) drv().ModuleUnload(m.second);
+  }
 };
 
 // ================================================================ C ABI
@@ -1823,6 +1837,7 @@ int bfa_batch_count(bfa_batch* bh, const int* ns, uint64_t* counts_dev, void* st
       CUfunction k;
       r = drv().ModuleGetFunction(&k, mod, "bfa_kernel");
       if (r != CUDA_SUCCESS) return set_err(BFA_E_JIT, "cuModuleGetFunction: %s", cu_str(r).c_str());
+      b->mod[dev] = mod;
       int nb = 1;
       drv().OccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, 256, 0);
       drv().FuncGetAttribute(&b->regs, CU_FUNC_ATTRIBUTE_NUM_REGS, k);

@@ -532,3 +532,24 @@ def test_c2_materialised():
         gw = host(p.eval_materialised(n, variant, count_out=cnt))
         assert np.array_equal(gw, ow) and int(cnt.item()) == oc
     assert p.count(n) == oc
+
+
+def test_programs_release_device_memory():
+    """Freeing a program unloads its JIT modules: compiling, running and
+    dropping many programs does not drift the device's free memory."""
+    import gc
+
+    def churn(k):
+        for s in range(k):
+            p = bfa.Program(W.random_dag(14, 60, seed=1000 + s))
+            p.set_option("graphs", 0)
+            p.count(14)
+            del p
+        gc.collect()
+        torch.cuda.synchronize()
+
+    churn(20)                                   # warm the allocators
+    free0 = torch.cuda.mem_get_info()[0]
+    churn(200)
+    free1 = torch.cuda.mem_get_info()[0]
+    assert free0 - free1 < 64 << 20, (free0 - free1) >> 20
