@@ -116,11 +116,13 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "kernel_cofactor_bits" count: split aligned sub-cubes into 2^j cofactor
  *                   programs, one kernel each (default 0; autotune sets it)
  *   "split_pieces"  count: Shannon-decompose aligned sub-cubes into this many
- *                   non-constant pieces first (default 0; autotune sets it)
+ *                   non-constant pieces first (0..65536; default 0; autotune sets it)
  *   "graphs"        replay multi-launch counts as CUDA graphs (default 1)
  *   "streams"       side streams for independent pieces / cofactors (default 4)
  *   "multi_body"    1: a split's cofactor children as one multi-body launch
  *                   (default 0)
+ *   "split_policy"  which piece split_pieces splits next: 0 the heaviest,
+ *                   1 the one whose best split saves the most work (default)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 

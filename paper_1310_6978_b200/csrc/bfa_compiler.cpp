@@ -415,8 +415,9 @@ uint32_t gate_count(const Parsed& p) {
   return g;
 }
 
-std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j) {
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total) {
   std::vector<int> chosen;
+  if (best_total) *best_total = UINT64_MAX;
   for (int step = 0; step < j; step++) {
     int best_v = -1;
     uint64_t best = UINT64_MAX;
@@ -436,6 +437,7 @@ std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j) {
     }
     if (best_v < 0) break;
     chosen.push_back(best_v);
+    if (best_total) *best_total = best;
   }
   return chosen;
 }
@@ -1281,6 +1283,46 @@ std::string emit_multi(const std::vector<const Parsed*>& progs, const std::vecto
   for (size_t c = 0; c < progs.size(); c++)
     os << "    case " << c << ": bfa_body_" << c << "(A, o_count, out_base_w, out, count, bid, bpc); break;\n";
   os << "  }\n}\n";
+  return os.str();
+}
+
+std::string emit_queue(const std::vector<std::string>& body_src, const std::vector<std::string>& body_name,
+                       const std::vector<uint64_t>& o_count, const std::vector<uint32_t>& chunks, int thread_bits,
+                       int min_blocks) {
+  std::ostringstream os;
+  const size_t nb = body_src.size();
+  os << "// generated by libbfa: work-queue kernel of " << nb << " programs\n" << kPrelude;
+  for (const std::string& b : body_src) os << b;
+  uint64_t total = 0;
+  os << "__constant__ u32 bfa_qpre[" << nb + 1 << "] = {";
+  for (size_t i = 0; i < nb; i++) {
+    os << (i ? ", " : "") << total << "u";
+    total += chunks[i];
+  }
+  os << ", " << total << "u};\n";
+  const std::string bounds = std::to_string(1 << thread_bits) + (min_blocks > 0 ? ", " + std::to_string(min_blocks) : "");
+  os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
+     << "bfa_kernel(u64* __restrict__ count, u32* __restrict__ ctr) {\n"
+     << "  __shared__ u32 s_chunk;\n"
+     << "  for (;;) {\n"
+     << "    __syncthreads();  // every thread has read the previous chunk number\n"
+     << "    if (threadIdx.x == 0) s_chunk = atomicAdd(ctr, 1u);\n"
+     << "    __syncthreads();\n"
+     << "    const u32 c = s_chunk;\n"
+     << "    if (c >= " << total << "u) {  // the last exit restores the counter for the next launch\n"
+     << "      if (threadIdx.x == 0 && c == " << total << "u + gridDim.x - 1u) *ctr = 0u;\n"
+     << "      return;\n"
+     << "    }\n"
+     << "    int lo = 0, hi = " << nb - 1 << ";\n"
+     << "    while (lo < hi) { const int mid = (lo + hi + 1) >> 1; if (bfa_qpre[mid] <= c) lo = mid; else hi = mid - 1; }\n"
+     << "    const u32 k = c - bfa_qpre[lo];\n"
+     << "    switch (lo) {\n";
+  for (size_t i = 0; i < nb; i++)
+    os << "      case " << i << ": " << body_name[i] << "(0ull, " << o_count[i] << "ull, 0ull, nullptr, count, k, "
+       << chunks[i] << "u); break;\n";
+  os << "    }\n"
+     << "  }\n"
+     << "}\n";
   return os.str();
 }
 

@@ -90,7 +90,7 @@ uint32_t gate_count(const Parsed& p);
 
 // Kernel-level cofactoring: greedily pick j of the variables < k whose
 // 2^j cofactors (bfa_assume) have the fewest gates in total after Reduction.
-std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j);
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total = nullptr);
 
 // ---------------------------------------------------------------- mapping
 struct Lut {
@@ -155,6 +155,21 @@ struct KernelStats {
 // signature: (u64 A, u64 o_count, u64 out_base_w, u32* out, u64* count, u32 bpc).
 std::string emit_multi(const std::vector<const Parsed*>& progs, const std::vector<KernelSpec>& specs,
                        std::vector<KernelStats>* stats);
+
+// One persistent work-queue kernel for many programs (the leaves of a
+// Shannon decomposition).  body_src[i] is the source of a noinline device
+// body named body_name[i] (emit_kernel with KernelSpec::body_name); body i
+// covers o_count[i] outer iterations, cut into chunks[i] contiguous chunks.
+// The chunks are numbered body by body in the given order; a block takes the
+// next chunk number with one atomicAdd on *ctr and runs that body on that
+// chunk, until all chunks are taken.  *ctr must be 0 before the first launch;
+// the block making the launch's last increment (total + gridDim.x - 1)
+// resets it to 0, so launches (and graph replays) need no memset, but two
+// launches of one module must not overlap in time.  Kernel signature:
+// (u64* count, u32* ctr).
+std::string emit_queue(const std::vector<std::string>& body_src, const std::vector<std::string>& body_name,
+                       const std::vector<uint64_t>& o_count, const std::vector<uint32_t>& chunks, int thread_bits,
+                       int min_blocks);
 
 // Modelled time per thread-iteration of the variant's best cover.
 double model_cost(const Parsed& prog, const KernelSpec& spec);

@@ -26,7 +26,10 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <atomic>
+#include <chrono>
 #include <mutex>
+#include <queue>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -302,6 +305,8 @@ struct Options {
   int graphs = 1;                // replay multi-launch counts as CUDA graphs
   int streams = 4;               // side streams for independent pieces / cofactors
   int multi_body = 0;            // 1: cofactor children of a piece as ONE multi-body launch (measured slower: occupancy of the largest child)
+  int split_policy = 1;          // 0: split the heaviest piece; 1: split the piece whose best split saves the most work
+  int queue_bodies = 0;          // > 0: decomposition leaves run as persistent work-queue kernels of <= this many bodies
 };
 
 struct JitEntry {
@@ -342,9 +347,28 @@ struct bfa_prog {
     uint64_t O = 0;
   };
   std::map<std::string, Multi> multis;
+  // work-queue kernels over decomposition leaves: key -> groups
+  struct QueueGroup {
+    std::string src_key;
+    std::vector<size_t> members;  // piece indices, in queue order
+    double l3 = 0, im = 0;        // executed cells per launch
+    uint32_t chunks = 0;
+  };
+  struct Queue {
+    std::vector<QueueGroup> groups;
+    size_t bodies = 0;
+    uint64_t chunks = 0;
+    double bodies_s = 0, nvrtc_s = 0;  // preparation: role searches + emission, NVRTC
+    std::vector<uint8_t> queued;  // per piece
+    std::map<int, uint32_t*> ctr; // per device: one self-resetting counter per group
+  };
+  std::map<std::string, Queue> queues;
+  std::map<std::string, double> decompose_s;  // host seconds per cached decomposition
   ~bfa_prog() {
     for (auto& g : graphs)
       if (g.second.second) cudaGraphExecDestroy(g.second.second);
+    for (auto& q : queues)
+      for (auto& c : q.second.ctr) cudaFree(c.second);
   }
 };
 
@@ -889,7 +913,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies;
   return k.str();
 }
 
@@ -1138,10 +1162,25 @@ int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, u
 // over ranks is the full count.
 int scratch_u64(int dev, uint64_t** p);
 
+// Run f(i) for i in [0, n) on the host's cores.
+template <class F>
+void parallel_for(size_t n, F f) {
+  const size_t W = std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency()));
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  for (size_t w = 0; w < W; w++)
+    th.emplace_back([&] {
+      for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+    });
+  for (auto& t : th) t.join();
+}
+
 struct Piece {
   std::unique_ptr<bfa_prog> prog;
   int nv = 0;
   uint64_t work = 0;
+  int split_v = -1;     // best single split variable (-1: not splittable)
+  uint64_t gain = 0;    // work saved by splitting on split_v
 };
 
 static uint64_t piece_work(const bfa_prog* q, int nv) {
@@ -1149,11 +1188,31 @@ static uint64_t piece_work(const bfa_prog* q, int nv) {
   return (uint64_t)(q->info.gates + 1) << std::min(nv, 40);
 }
 
-// Shannon decomposition of `base` (nv free variables): split the heaviest
-// non-constant piece by its own best variable until `target` non-constant
-// pieces exist (or no piece has more than 24 variables).  Pieces inherit p's
-// options (incl. kernel_cofactor_bits, applied inside each piece).
+// The piece's best single split (the variable whose two cofactors have the
+// fewest gates in total) and the work it saves.
+static void score_split(Piece* x) {
+  x->split_v = -1;
+  x->gain = 0;
+  if (x->work == 0 || x->nv <= 24) return;
+  uint64_t total = 0;
+  std::vector<int> J = bfa::choose_cofactor_vars(x->prog->parsed, x->nv, 1, &total);
+  if (J.empty()) return;
+  x->split_v = J[0];
+  const uint64_t after = (total + 2) << std::min(x->nv - 1, 40);
+  x->gain = x->work > after ? x->work - after : 0;
+}
+
+// Shannon decomposition of `base` (nv free variables) into `target`
+// non-constant pieces ("further partition").
+// Every step splits one piece on its own best variable (both cofactors via
+// bfa_assume + Reduction), so different branches split on different
+// variables.  Policy 0 splits the heaviest piece (work = (gates + 1) x
+// 2^free_vars); policy 1 (default) splits the piece whose split saves the
+// most work, ties to the heaviest.  Pieces with <= 24 free variables are not
+// split.  Pieces inherit p's options (incl. kernel_cofactor_bits, applied
+// inside each piece).
 std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed base, int nv, int target) {
+  const int policy = p->opt.split_policy;
   std::vector<Piece> pieces;
   {
     Piece root;
@@ -1163,27 +1222,64 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
     fill_info(root.prog.get());
     root.nv = nv;
     root.work = piece_work(root.prog.get(), nv);
+    if (policy == 1) score_split(&root);
     pieces.push_back(std::move(root));
   }
-  auto nonconst = [&] { int c = 0; for (auto& x : pieces) c += x.work > 0; return c; };
-  for (int guard = 0; guard < 4096 && nonconst() < target; guard++) {
-    size_t h = pieces.size();
-    for (size_t i = 0; i < pieces.size(); i++)
-      if (pieces[i].work > 0 && pieces[i].nv > 24 && (h == pieces.size() || pieces[i].work > pieces[h].work)) h = i;
-    if (h == pieces.size()) break;
-    Piece big = std::move(pieces[h]);
-    pieces.erase(pieces.begin() + h);
-    std::vector<int> J = bfa::choose_cofactor_vars(big.prog->parsed, big.nv, 1);
-    const int v = J.empty() ? 0 : J[0];
-    for (int b = 0; b < 2; b++) {
-      Piece c;
+  // max-heap of splittable pieces; ties go to the lower index (deterministic)
+  auto key = [&](size_t i) {
+    const Piece& x = pieces[i];
+    return policy == 1 ? std::make_pair(x.gain, x.work) : std::make_pair(x.work, (uint64_t)0);
+  };
+  auto less = [&](size_t a, size_t b) { auto ka = key(a), kb = key(b); return ka != kb ? ka < kb : a > b; };
+  std::priority_queue<size_t, std::vector<size_t>, decltype(less)> heap(less);
+  auto splittable = [&](size_t i) {
+    const Piece& x = pieces[i];
+    return x.work > 0 && x.nv > 24 && (policy == 0 || x.split_v >= 0);
+  };
+  if (splittable(0)) heap.push(0);
+  int live = pieces[0].work > 0;
+  // pieces are split in batches (the top of the heap, at most one per host
+  // core and no more than the target still needs), the splits of a batch in
+  // parallel; the batches depend only on the heap, so every rank gets the same
+  // decomposition
+  const size_t cores = std::max(1u, std::thread::hardware_concurrency());
+  while (live < target && !heap.empty()) {
+    std::vector<size_t> batch;
+    while (!heap.empty() && batch.size() < cores && live - (int)batch.size() + 2 * (int)(batch.size() + 1) <= target + 1) {
+      batch.push_back(heap.top());
+      heap.pop();
+    }
+    if (batch.empty()) { batch.push_back(heap.top()); heap.pop(); }
+    std::vector<Piece> kid(2 * batch.size());
+    std::vector<Piece> big(batch.size());
+    for (size_t e = 0; e < batch.size(); e++) {
+      big[e] = std::move(pieces[batch[e]]);
+      live--;
+    }
+    parallel_for(2 * batch.size(), [&](size_t q) {
+      const Piece& par = big[q / 2];
+      const int b = (int)(q & 1);
+      int v = par.split_v;
+      if (policy == 0) {
+        std::vector<int> J = bfa::choose_cofactor_vars(par.prog->parsed, par.nv, 1);
+        v = J.empty() ? 0 : J[0];
+      }
+      Piece& c = kid[q];
       c.prog = std::make_unique<bfa_prog>();
-      c.prog->parsed = bfa::assume(big.prog->parsed, big.nv, 1ull << v, (uint64_t)b << v, nullptr);
+      c.prog->parsed = bfa::assume(par.prog->parsed, par.nv, 1ull << v, (uint64_t)b << v, nullptr);
       c.prog->opt = p->opt;
       fill_info(c.prog.get());
-      c.nv = big.nv - 1;
+      c.nv = par.nv - 1;
       c.work = piece_work(c.prog.get(), c.nv);
-      pieces.insert(pieces.begin() + h + b, std::move(c));
+      if (policy == 1) score_split(&c);
+    });
+    for (size_t e = 0; e < batch.size(); e++) {
+      const size_t h = batch[e];
+      for (int b = 0; b < 2; b++) live += kid[2 * e + b].work > 0;
+      pieces[h] = std::move(kid[2 * e]);        // cofactor 0 takes the parent's slot,
+      pieces.push_back(std::move(kid[2 * e + 1]));  // cofactor 1 goes to the end
+      if (splittable(h)) heap.push(h);
+      if (splittable(pieces.size() - 1)) heap.push(pieces.size() - 1);
     }
   }
   std::vector<std::unique_ptr<bfa_prog>> made;
@@ -1214,7 +1310,8 @@ int prepare_split(const bfa_prog* p, int nv, int sms) {
 
 // Count the pieces owned by `rank` (owner[i] == rank) into count_dev (written).
 int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
-                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out);
+                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out, bfa_prog* holder,
+                 const std::string& qkey);
 
 // The sharding plan (host only, deterministic): pieces of the cube and the
 // rank owning each (LPT on the estimated work).
@@ -1277,7 +1374,11 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
   DevInfo di;
   if ((rc = current_device(&dev, &di))) return rc;
   int kernels = 0;
-  auto body = [&](cudaStream_t s) { return count_pieces(*plan.kids, plan.owner, rank, dev, di.sms, count_dev, s, &kernels); };
+  const std::string qkey = "q." + std::to_string(n) + "." + std::to_string(rank) + "." + std::to_string(world) + "." +
+                           options_key(p->opt);
+  auto body = [&](cudaStream_t s) {
+    return count_pieces(*plan.kids, plan.owner, rank, dev, di.sms, count_dev, s, &kernels, const_cast<bfa_prog*>(p), qkey);
+  };
   if (p->opt.graphs) {
     std::ostringstream k;
     k << "shard|" << dev << '.' << n << '.' << rank << '.' << world << '.' << (uintptr_t)count_dev << '|'
@@ -1299,21 +1400,161 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
   return BFA_OK;
 }
 
+// The work-queue kernels over the pieces `rank` owns (host side, built once
+// per key): every eligible piece (non-constant, no further cofactor split, a
+// specialised whole-cube plan) becomes a noinline body with the FULL inner
+// loop (no piece has to fill the GPU alone, so none gives up loop-invariant
+// hoisting); the bodies, sorted by their per-iteration cell count (a proxy of
+// their register need), are cut into groups of <= queue_bodies bodies and
+// about equal estimated work (NVRTC time grows faster than linearly with a
+// module's size, and groups compile in parallel); within a group the heaviest bodies come first and every body is cut
+// into chunks of about equal work, 32 per SM per group.
+int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::unique_ptr<bfa_prog>>& kids,
+                 const std::vector<int>& owner, int rank, int sms, bfa_prog::Queue** out) {
+  {
+    std::lock_guard<std::mutex> lk(holder->mu);
+    auto it = holder->queues.find(key);
+    if (it != holder->queues.end()) { *out = &it->second; return BFA_OK; }
+  }
+  const Options& o = holder->opt;
+  const int s = o.slot_bits, t = o.thread_bits;
+  std::vector<size_t> elig;
+  for (size_t i = 0; i < kids.size(); i++) {
+    const bfa_prog* q = kids[i].get();
+    const int nv = q->piece_nv;
+    if (owner[i] != rank || q->info.const_value == 0 || q->opt.kernel_cofactor_bits > 0 || q->opt.force_generic ||
+        q->opt.engine || q->opt.segment_cells || q->info.luts > 8000 || nv > 63 || nv < 5 + s + t)
+      continue;
+    elig.push_back(i);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  struct Body {
+    std::string name, src;
+    bfa::KernelStats st;
+    uint64_t O = 0;
+    int m = 0, nv = 0;
+    double cost = 0, size = 0;
+  };
+  std::vector<Body> B(elig.size());
+  parallel_for(elig.size(), [&](size_t e) {
+    const size_t i = elig[e];
+    bfa_prog* q = kids[i].get();
+    Body& b = B[e];
+    b.nv = q->piece_nv;
+    b.m = std::min(o.inner_bits, b.nv - 5 - s - t);
+    bfa::KernelSpec spec;
+    spec.mode = bfa::KM_COUNT; spec.generic = false; spec.slot_bits = s; spec.thread_bits = t;
+    spec.inner_bits = b.m; spec.dual_pipe = o.dual_pipe; spec.imad_cost_pct = o.imad_cost_pct;
+    spec.min_blocks = o.min_blocks;
+    resolve_roles(q, &spec, b.nv);
+    b.name = "bfa_body_" + std::to_string(i);
+    spec.body_name = b.name;
+    b.src = bfa::emit_kernel(q->parsed, spec, &b.st);
+    b.O = (1ull << (b.nv - 5)) >> (s + t + b.m);
+    const double inner = b.st.luts_inner + b.st.imads_inner + b.st.derived_inner;
+    const double outer = b.st.luts_outer + b.st.imads_outer + b.st.derived_outer;
+    b.size = inner;
+    b.cost = (double)b.O * (std::ldexp(inner + 2.0 * (1 << s) + 6.0, b.m) + outer + 12.0);
+  });
+  bfa_prog::Queue Q;
+  Q.queued.assign(kids.size(), 0);
+  Q.bodies = elig.size();
+  const auto t1 = std::chrono::steady_clock::now();
+  Q.bodies_s = std::chrono::duration<double>(t1 - t0).count();
+  const int G = (int)((elig.size() + std::max(1, o.queue_bodies) - 1) / std::max(1, o.queue_bodies));
+  std::vector<size_t> order(elig.size());
+  for (size_t e = 0; e < order.size(); e++) order[e] = e;
+  std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return B[x].size > B[y].size; });
+  double total = 0;
+  for (const Body& b : B) total += b.cost;
+  std::vector<std::vector<size_t>> groups(std::max(G, 0));
+  {
+    double run = 0;
+    int g = 0;
+    for (size_t r = 0; r < order.size(); r++) {
+      const int gw = (int)std::min<double>(G - 1, std::floor(run / std::max(total, 1e-30) * G));
+      if ((gw > g || (int)groups[g].size() >= o.queue_bodies) && g + 1 < G) g++;
+      groups[g].push_back(order[r]);
+      run += B[order[r]].cost;
+    }
+    // the work boundaries can leave more than queue_bodies in the last group
+    while (!groups.empty() && (int)groups.back().size() > o.queue_bodies) {
+      std::vector<size_t> tail(groups.back().begin() + o.queue_bodies, groups.back().end());
+      groups.back().resize(o.queue_bodies);
+      groups.push_back(std::move(tail));
+    }
+  }
+  std::vector<std::string> srcs;
+  for (auto& gm : groups) {
+    if (gm.empty()) continue;
+    std::stable_sort(gm.begin(), gm.end(), [&](size_t x, size_t y) { return B[x].cost > B[y].cost; });
+    double gcost = 0;
+    for (size_t e : gm) gcost += B[e].cost;
+    const double target = 32.0 * sms;
+    std::vector<std::string> bsrc, bname;
+    std::vector<uint64_t> O;
+    std::vector<uint32_t> ch;
+    bfa_prog::QueueGroup qg;
+    for (size_t e : gm) {
+      const Body& b = B[e];
+      const double want = std::llround(target * b.cost / std::max(gcost, 1e-30));
+      const uint32_t c = (uint32_t)std::max<double>(1.0, std::min<double>((double)b.O, want));
+      bsrc.push_back(b.src);
+      bname.push_back(b.name);
+      O.push_back(b.O);
+      ch.push_back(c);
+      qg.members.push_back(elig[e]);
+      qg.chunks += c;
+      Q.queued[elig[e]] = 1;
+      const double S = 1 << s, it = std::ldexp(1.0, b.m), words = std::ldexp(1.0, b.nv - 5);
+      qg.l3 += words * (b.st.luts_inner / S + b.st.luts_outer / (S * it));
+      qg.im += words * ((b.st.imads_inner + b.st.derived_inner) / S +
+                        (b.st.imads_outer + b.st.derived_outer) / (S * it));
+    }
+    srcs.push_back(bfa::emit_queue(bsrc, bname, O, ch, t, o.min_blocks));
+    qg.src_key = key + "|g" + std::to_string(Q.groups.size());
+    Q.chunks += qg.chunks;
+    Q.groups.push_back(std::move(qg));
+  }
+  std::vector<int> rcs(srcs.size(), BFA_OK);
+  parallel_for(srcs.size(), [&](size_t g) {
+    rcs[g] = get_kernel_src(holder, Q.groups[g].src_key, srcs[g], t, -1, nullptr, nullptr);  // NVRTC (cached)
+  });
+  for (int r : rcs)
+    if (r) return r;
+  Q.nvrtc_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  std::lock_guard<std::mutex> lk(holder->mu);
+  auto it = holder->queues.find(key);
+  if (it == holder->queues.end()) it = holder->queues.emplace(key, std::move(Q)).first;
+  *out = &it->second;
+  return BFA_OK;
+}
+
+thread_local std::string g_queue_report;  // the last count_pieces' work-queue summary (JSON object or empty)
+
 int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int dev,
-                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out) {
+                 int sms, uint64_t* count_dev, cudaStream_t st, int* kernels_out, bfa_prog* holder,
+                 const std::string& qkey) {
+  g_queue_report.clear();
   cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
   if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  bfa_prog::Queue* Q = nullptr;
+  if (holder && holder->opt.queue_bodies > 0) {
+    int rc = ensure_queue(holder, qkey, kids, owner, rank, sms, &Q);
+    if (rc) return rc;
+  }
+  auto queued = [&](size_t i) { return Q && Q->queued[i]; };
   {  // compile the owned pieces' kernels in parallel (pieces that split
      // further into cofactor kernels prepare their own children)
-    std::vector<std::thread> th;
-    std::vector<int> rcs(kids.size(), 0);
+    std::vector<size_t> todo;
     for (size_t i = 0; i < kids.size(); i++)
-      if (owner[i] == rank && kids[i]->info.const_value != 0)
-        th.emplace_back([&, i] {
-          rcs[i] = kids[i]->opt.kernel_cofactor_bits == 0 ? prepare_count(kids[i].get(), kids[i]->piece_nv, sms)
-                                                          : prepare_split(kids[i].get(), kids[i]->piece_nv, sms);
-        });
-    for (auto& t : th) t.join();
+      if (owner[i] == rank && kids[i]->info.const_value != 0 && !queued(i)) todo.push_back(i);
+    std::vector<int> rcs(todo.size(), 0);
+    parallel_for(todo.size(), [&](size_t e) {
+      const size_t i = todo[e];
+      rcs[e] = kids[i]->opt.kernel_cofactor_bits == 0 ? prepare_count(kids[i].get(), kids[i]->piece_nv, sms)
+                                                      : prepare_split(kids[i].get(), kids[i]->piece_nv, sms);
+    });
     for (int r : rcs) if (r) return r;
   }
   // every piece adds into count_dev (a piece that splits into its own
@@ -1322,8 +1563,42 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
   double l3 = 0, im = 0, decided = 0;
   int rc = BFA_OK;
   Fork fork(st, dev);
+  if (Q) {
+    uint32_t* ctr = nullptr;
+    {
+      std::lock_guard<std::mutex> lk(holder->mu);
+      auto c = Q->ctr.find(dev);
+      if (c != Q->ctr.end()) ctr = c->second;
+    }
+    if (!ctr && !Q->groups.empty()) {
+      const size_t bytes = Q->groups.size() * sizeof(uint32_t);
+      if (cudaMalloc(&ctr, bytes) != cudaSuccess) return set_err(BFA_E_NOMEM, "queue counters");
+      if (cudaMemset(ctr, 0, bytes) != cudaSuccess) return set_err(BFA_E_CUDA, "queue counters");
+      std::lock_guard<std::mutex> lk(holder->mu);
+      Q->ctr[dev] = ctr;
+    }
+    const int T = 1 << holder->opt.thread_bits;
+    std::ostringstream qr;
+    qr << "{\"modules\": " << Q->groups.size() << ", \"bodies\": " << Q->bodies << ", \"chunks\": " << Q->chunks
+       << ", \"bodies_s\": " << Q->bodies_s << ", \"nvrtc_s\": " << Q->nvrtc_s << "}";
+    g_queue_report = qr.str();
+    for (size_t g = 0; g < Q->groups.size(); g++) {
+      auto& qg = Q->groups[g];
+      JitEntry* je = nullptr;
+      CUfunction fn;
+      if ((rc = get_kernel_src(holder, qg.src_key, "", holder->opt.thread_bits, dev, &je, &fn))) return rc;
+      unsigned grid = (unsigned)std::min<uint64_t>(qg.chunks, (uint64_t)sms * je->occupancy[dev]);
+      uint64_t* cnt = count_dev;
+      uint32_t* c = ctr + g;
+      void* args[] = {&cnt, &c};
+      if ((rc = launch(fn, grid, T, fork.stream(), args))) return rc;
+      l3 += qg.l3;
+      im += qg.im;
+      kernels++;
+    }
+  }
   for (size_t i = 0; i < kids.size(); i++) {
-    if (owner[i] != rank) continue;
+    if (owner[i] != rank || queued(i)) continue;
     const int nv = kids[i]->piece_nv;
     if (kids[i]->info.const_value == 0) { decided += (double)(1ull << nv); continue; }
     g_cells_lop3 = g_cells_imad = 0;
@@ -1362,7 +1637,8 @@ int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* c
   const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
   const uint64_t top_vals = mu_lo & top_mask;
   const std::string key = "split." + std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) +
-                          "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits);
+                          "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits) +
+                          "." + std::to_string(p->opt.split_policy);
   std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
   {
     std::lock_guard<std::mutex> lk(mp->mu);
@@ -1370,24 +1646,33 @@ int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* c
     if (it != mp->cofactors.end()) kids = &it->second;
   }
   if (!kids) {
+    const auto t0 = std::chrono::steady_clock::now();
     std::vector<std::unique_ptr<bfa_prog>> made =
         decompose(p, bfa::assume(p->parsed, n, top_mask, top_vals, nullptr), k, p->opt.split_pieces);
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     std::lock_guard<std::mutex> lk(mp->mu);
     auto it = mp->cofactors.find(key);
     if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
     kids = &it->second;
+    mp->decompose_s[key] = secs;
   }
   std::vector<int> owner(kids->size(), 0);
   int kernels = 0, zero = 0;
   uint64_t zero_vals = 0;
   for (auto& q : *kids)
     if (q->info.const_value == 0) { zero++; zero_vals += 1ull << q->piece_nv; }
-  if ((rc = count_pieces(*kids, owner, 0, dev, di.sms, count_dev, st, &kernels))) return rc;
+  if ((rc = count_pieces(*kids, owner, 0, dev, di.sms, count_dev, st, &kernels, mp, "q." + key))) return rc;
   std::ostringstream js;
   (void)zero_vals;
   js << "{\"variant\": \"decomposed\", \"pieces\": " << kids->size() << ", \"constant_zero\": " << zero
      << ", \"valuations_decided\": " << g_decided << ", \"kernels\": " << kernels << ", \"cells_lop3\": "
-     << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad << "}";
+     << g_cells_lop3 << ", \"cells_imad\": " << g_cells_imad;
+  {
+    std::lock_guard<std::mutex> lk(mp->mu);
+    js << ", \"decompose_s\": " << mp->decompose_s[key];
+  }
+  if (!g_queue_report.empty()) js << ", \"queue\": " << g_queue_report;
+  js << "}";
   g_last_launch = js.str();
   return BFA_OK;
 }
@@ -1564,10 +1849,12 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }
   else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
   else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }
-  else if (k == "split_pieces") { if (v < 0 || v > 1024) return bad(); p->opt.split_pieces = (int)v; }
+  else if (k == "split_pieces") { if (v < 0 || v > 65536) return bad(); p->opt.split_pieces = (int)v; }
   else if (k == "graphs") { if (v < 0 || v > 1) return bad(); p->opt.graphs = (int)v; }
   else if (k == "streams") { if (v < 1 || v > 16) return bad(); p->opt.streams = (int)v; }
   else if (k == "multi_body") { if (v < 0 || v > 1) return bad(); p->opt.multi_body = (int)v; }
+  else if (k == "split_policy") { if (v < 0 || v > 1) return bad(); p->opt.split_policy = (int)v; }
+  else if (k == "queue_bodies") { if (v < 0 || v > 8192) return bad(); p->opt.queue_bodies = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -1711,28 +1998,35 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   cudaError_t ce = cudaStreamSynchronize(st);
   if (ce != cudaSuccess) { p->opt = base; return set_err(BFA_E_CUDA, "autotune: %s", cudaGetErrorString(ce)); }
   p->opt = best >= 0 ? cands[best].o : base;
-  // phase 3: kernel-level cofactoring (count mode over the whole sub-cube the
+  // phase 3: partial evaluation (count mode over the whole sub-cube the
   // caller will count: 2^k_free valuations when that takes <= ~2 s, else the
-  // probe).  Each j splits into 2^j cofactor programs (prepared once, cached).
-  std::vector<std::pair<int, float>> kcof;
+  // probe).  Stage A: kernel-level cofactoring, 2^j cofactor kernels.  Stage
+  // Q: a Shannon decomposition into split_pieces leaves run as work-queue
+  // kernels of <= 512 bodies, 4096 and 16384 leaves (32768 when 16384 won and
+  // prepared in under a minute); only when the whole count takes > 1 ms.
+  struct Trial { int sp, j, qb; float ms; double prep_s; };
+  std::vector<Trial> kcof;
   if (best >= 0 && k_free >= 28) {
     const double est = cands[best].ms * std::pow(2.0, k_free - k);
     uint64_t tlo = lo, thi = hi;
     if (est <= 2000.0 && k_free == n) { tlo = 0; thi = hi; }
     else if (est <= 2000.0) { thi = hi; tlo = hi - (1ull << k_free); }
-    int best_j = 0, best_sp = 0;
-    float best_ms = 1e30f;
-    auto trial = [&](int sp, int jj) -> int {
+    Trial bestt{0, 0, 0, 1e30f, 0};
+    auto trial = [&](int sp, int jj, int qb) -> int {
       if (jj < 0 || jj > 8) return BFA_OK;
       for (auto& done : kcof)
-        if (done.first == jj + 100 * sp) return BFA_OK;
+        if (done.sp == sp && done.j == jj && done.qb == qb) return BFA_OK;
       if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj + (sp ? 4 : 0)) return BFA_OK;
       p->opt.kernel_cofactor_bits = jj;
       p->opt.split_pieces = sp;
+      p->opt.queue_bodies = qb;
+      const auto t0 = std::chrono::steady_clock::now();
       int r2 = run_range(p, n, tlo, thi, nullptr, d, st, false);
       if (r2) return r2;
+      cudaStreamSynchronize(st);
+      const double prep = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       float bm = 1e30f;
-      for (int r = 0; r < 2; r++) {
+      for (int r = 0; r < 3; r++) {  // direct, graph capture + replay, replay
         cudaEventRecord(e0, st);
         run_range(p, n, tlo, thi, nullptr, d, st, false);
         cudaEventRecord(e1, st);
@@ -1741,27 +2035,21 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
         cudaEventElapsedTime(&ms, e0, e1);
         bm = std::min(bm, ms);
       }
-      kcof.push_back({jj + 100 * sp, bm});
-      if (bm < best_ms) { best_ms = bm; best_j = jj; best_sp = sp; }
+      kcof.push_back({sp, jj, qb, bm, prep});
+      if (bm < bestt.ms) bestt = kcof.back();
       return BFA_OK;
     };
-    // stage A: cofactor bits without pieces; B: Shannon pieces at ~ the same
-    // total split depth; C: refine around the best
-    for (int jj : {0, 2, 4, 6})
-      if ((rc = trial(0, jj))) break;
-    const int ja = best_j;
-    if (!rc && ja > 0) {
-      for (auto tr : {std::make_pair(16, ja - 1), std::make_pair(64, ja - 2)})
-        if ((rc = trial(tr.first, tr.second))) break;
-      if (!rc && best_sp > 0) {
-        const int sp = best_sp, jb = best_j;
-        for (auto tr : {std::make_pair(sp, jb + 1), std::make_pair(sp * 2, jb)})
-          if ((rc = trial(tr.first, tr.second))) break;
-      }
+    for (int jj : {0, 4})
+      if ((rc = trial(0, jj, 0))) break;
+    if (!rc && bestt.ms > 1.0f) {
+      for (int sp : {4096, 16384})
+        if ((rc = trial(sp, 0, 512))) break;
+      if (!rc && bestt.sp == 16384 && kcof.back().prep_s < 60.0) rc = trial(32768, 0, 512);
     }
     if (rc) p->opt = cands[best].o;
-    p->opt.kernel_cofactor_bits = best_j;
-    p->opt.split_pieces = best_sp;
+    p->opt.kernel_cofactor_bits = bestt.j;
+    p->opt.split_pieces = bestt.sp;
+    p->opt.queue_bodies = bestt.qb;
   }
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
@@ -1779,10 +2067,10 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
      << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
      << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits
      << ", \"kernel_cofactor_bits\": " << p->opt.kernel_cofactor_bits << ", \"split_pieces\": " << p->opt.split_pieces
-     << "}, \"kernel_cofactoring\": [";
+     << ", \"queue_bodies\": " << p->opt.queue_bodies << "}, \"partial_evaluation\": [";
   for (size_t i = 0; i < kcof.size(); i++)
-    js << (i ? ", " : "") << "{\"split_pieces\": " << kcof[i].first / 100 << ", \"j\": " << kcof[i].first % 100
-       << ", \"ms\": " << kcof[i].second << "}";
+    js << (i ? ", " : "") << "{\"split_pieces\": " << kcof[i].sp << ", \"j\": " << kcof[i].j << ", \"queue_bodies\": "
+       << kcof[i].qb << ", \"ms\": " << kcof[i].ms << ", \"prep_s\": " << kcof[i].prep_s << "}";
   js << "]}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
   return BFA_OK;

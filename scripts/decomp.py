@@ -36,5 +36,9 @@ for spec in sys.argv[3:]:
     torch.cuda.synchronize()
     c = int(cnt.item())
     ref = c if ref is None else ref
+    ll = bfa.last_launch()
+    l3, im = ll.get("cells_lop3", 0), ll.get("cells_imad", 0)
+    floor = max(l3 / 18.6e12, (l3 + im) / 35.2e12) * 1e3   # ALU-pipe / issue bound, ms
     print(json.dumps({"sp": sp, "j": j, "ms": round(s.elapsed_time(e) / 5, 3), "ok": c == ref, "prep_s": round(prep, 1),
-                      "decided": bfa.last_launch().get("valuations_decided")}), flush=True)
+                      "count": c, "decided": ll.get("valuations_decided"), "kernels": ll.get("kernels"),
+                      "cells_lop3": l3, "cells_imad": im, "alu_floor_ms": round(floor, 3)}), flush=True)

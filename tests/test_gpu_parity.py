@@ -311,6 +311,41 @@ def test_split_pieces():
         int(bfa.Program(text).count_range(n, lo, lo + (1 << 32)).item())
 
 
+def test_work_queue_kernels():
+    """Decomposition leaves run as persistent work-queue kernels (blocks take
+    equal-work chunks of many noinline bodies with an atomic counter that the
+    last block resets): counts equal the plain kernel's on the full cube, on
+    an aligned sub-cube, over direct / captured / replayed calls, for one body
+    per module up to all bodies in one module, and f + ~f fills the cube."""
+    for cfg in ("c4", "c5"):
+        text, n, _ = W.config(cfg)
+        full = bfa.Program(text).count(n)
+        for sp, qb in ((64, 1), (256, 16), (1024, 512)):
+            p = bfa.Program(text).set_option("split_pieces", sp).set_option("queue_bodies", qb)
+            out = torch.zeros(1, dtype=torch.int64, device="cuda")
+            for _ in range(4):                   # direct, graph capture, replays
+                p.count_range(n, 0, 1 << n, out=out)
+                assert int(out.item()) == full, (cfg, sp, qb)
+            ll = bfa.last_launch()
+            assert ll["variant"] == "decomposed" and ll["queue"]["bodies"] > 0
+            assert ll["queue"]["modules"] >= -(-ll["queue"]["bodies"] // qb)
+            assert p.count(n) == full
+    text, n, _ = W.config("c5")
+    body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+    lo = 5 << 32
+    ref = int(bfa.Program(text).count_range(n, lo, lo + (1 << 32)).item())
+    p = bfa.Program(text).set_option("split_pieces", 512).set_option("queue_bodies", 64)
+    pc = bfa.Program(f"{body}\n~{out}").set_option("split_pieces", 512).set_option("queue_bodies", 64)
+    a = int(p.count_range(n, lo, lo + (1 << 32)).item())
+    assert a == ref
+    assert a + int(pc.count_range(n, lo, lo + (1 << 32)).item()) == 1 << 32
+    p = bfa.Program(text).set_option("split_pieces", 256).set_option("queue_bodies", 32)
+    full = bfa.Program(text).count(n)
+    for world in (2, 4):
+        shares = [int(p.count_shard(n, r, world).item()) for r in range(world)]
+        assert sum(shares) == full
+
+
 def test_graph_replay():
     """Multi-launch counts replay as CUDA graphs from the third call on:
     results and the launch counter stay exact across direct, captured and
