@@ -123,6 +123,12 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   (default 0)
  *   "split_policy"  which piece split_pieces splits next: 0 the heaviest,
  *                   1 the one whose best split saves the most work (default)
+ *   "queue_bodies"  > 0: the leaves of a split_pieces decomposition run as
+ *                   persistent work-queue kernels of at most this many
+ *                   bodies each (default 0 = one kernel per leaf; autotune
+ *                   sets it)
+ *   "queue_chunk"   work-queue chunk size in modelled thread-instructions
+ *                   (default 65536)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 
@@ -174,6 +180,14 @@ int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* cou
  * rank computes the same plan. */
 int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_vars, uint64_t* work, int capacity,
                    int* n_pieces);
+
+/* Host-only preparation (SURVEY.md §8(b) bfa_compile's JIT, ahead of time):
+ * everything bfa_count(p, n) compiles before its first launch -- the
+ * decomposition, role searches, kernel emission and NVRTC -- for a device
+ * with `sms` SMs (<= 0: the current device's, else 148).  Needs no GPU and
+ * launches nothing; results are cached in p (and in the persistent JIT cache).
+ * Returns BFA_OK, BFA_E_RANGE (bad n) or BFA_E_JIT. */
+int bfa_prepare(const bfa_prog* p, int n, int sms);
 
 /* The slice [mu_lo, mu_hi) of the DNF vector, asynchronously on `stream`:
  * bit (mu - mu_lo) at word (mu - mu_lo) >> 6 of out_dev (device,

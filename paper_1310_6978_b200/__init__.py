@@ -53,6 +53,7 @@ _SIGS = {
     "bfa_count_shard": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.c_void_p, _c.c_void_p]),
     "bfa_shard_plan": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                   _c.POINTER(_c.c_uint64), _c.c_int, _c.POINTER(_c.c_int)]),
+    "bfa_prepare": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int]),
     "bfa_last_error": (_c.c_char_p, []),
     "bfa_version": (_c.c_char_p, []),
 }
@@ -176,6 +177,12 @@ class Program:
         out = _u64_out(out, 1)
         _check(_load().bfa_count_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
         return out
+
+    def prepare(self, n: int, sms: int = 0):
+        """bfa_prepare (host only, no GPU needed): compile everything count(n)
+        needs before its first launch; returns self."""
+        _check(_load().bfa_prepare(self._h, n, sms))
+        return self
 
     def count_shard(self, n: int, rank: int, world: int, out=None, stream=None):
         """bfa_count_shard: this rank's share of the count under work-balanced

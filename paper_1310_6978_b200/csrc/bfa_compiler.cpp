@@ -733,13 +733,15 @@ struct Emitter {
   }
 };
 
+}  // namespace
+
 const char* kPrelude =
     "typedef unsigned int u32;\n"
     "typedef unsigned long long u64;\n"
     "struct __align__(16) u32x4 { u32 x, y, z, w; };\n"
     "struct __align__(8) u32x2 { u32 x, y; };\n"
     "// enumerate mode: append the valuations of the set bits of word w\n"
-    "__device__ __forceinline__ void bfa_append(u32 r, u64 w, u64* cursor, u64* mu_out, u64 cap) {\n"
+    "static __device__ __forceinline__ void bfa_append(u32 r, u64 w, u64* cursor, u64* mu_out, u64 cap) {\n"
     "  if (!r) return;\n"
     "  u64 pos = atomicAdd(cursor, (u64)__popc(r));\n"
     "  while (r) {\n"
@@ -749,7 +751,13 @@ const char* kPrelude =
     "    ++pos;\n"
     "  }\n"
     "}\n"
-    "__device__ __forceinline__ void bfa_block_sum(u64 acc, u64* count) {\n"
+    "// per-warp sum, one atomic per warp (device bodies: no block barrier, no static shared memory)\n"
+    "static __device__ __forceinline__ void bfa_warp_sum(u64 acc, u64* count) {\n"
+    "  #pragma unroll\n"
+    "  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
+    "  if ((threadIdx.x & 31u) == 0 && acc) atomicAdd(count, acc);\n"
+    "}\n"
+    "static __device__ __forceinline__ void bfa_block_sum(u64 acc, u64* count) {\n"
     "  #pragma unroll\n"
     "  for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);\n"
     "  __shared__ u64 red[32];\n"
@@ -764,7 +772,6 @@ const char* kPrelude =
     "  }\n"
     "}\n";
 
-}  // namespace
 
 // The specialised DAG of one kernel variant: the 2^s slot cofactors of f
 // with lane words as constants, and the loop level of every variable from
@@ -1053,7 +1060,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   } else {
     const int unit = s + t + m;
     if (as_body)
-      os << "__device__ __noinline__ void " << spec.body_name
+      os << "extern \"C\" __device__ __noinline__ void " << spec.body_name
          << "(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
          << enum_params << ", const u32 bid_, const u32 nb_) {\n";
     else
@@ -1112,7 +1119,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     os << "    }\n"
        << "    acc += acc32;\n"
        << "  }\n";
-    if (want_count) os << "  bfa_block_sum(acc, count);\n";
+    if (want_count) os << (as_body ? "  bfa_warp_sum(acc, count);\n" : "  bfa_block_sum(acc, count);\n");
     os << "}\n";
     st.words_per_iter = (uint32_t)S;
   }

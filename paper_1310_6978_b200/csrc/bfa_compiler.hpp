@@ -171,6 +171,9 @@ std::string emit_queue(const std::vector<std::string>& body_src, const std::vect
                        const std::vector<uint64_t>& o_count, const std::vector<uint32_t>& chunks, int thread_bits,
                        int min_blocks);
 
+// Common device helpers of every generated source (typedefs, sums, append).
+extern const char* kPrelude;
+
 // Modelled time per thread-iteration of the variant's best cover.
 double model_cost(const Parsed& prog, const KernelSpec& spec);
 

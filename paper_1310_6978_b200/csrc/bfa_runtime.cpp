@@ -29,6 +29,7 @@
 #include <atomic>
 #include <chrono>
 #include <mutex>
+#include <set>
 #include <queue>
 #include <sstream>
 #include <string>
@@ -202,7 +203,18 @@ int current_device(int* dev, DevInfo* info) {
 }
 
 // ------------------------------------------------------------ NVRTC
+uint64_t fnv64(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* c = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < n; i++) { h ^= c[i]; h *= 1099511628211ull; }
+  return h;
+}
+
 int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
+  if (const char* dir = getenv("BFA_DUMP_SRC")) {  // debugging: keep every generated source
+    char path[4096];
+    snprintf(path, sizeof path, "%s/%016llx.cu", dir, (unsigned long long)fnv64(src.data(), src.size()));
+    if (FILE* f = fopen(path, "w")) { fwrite(src.data(), 1, src.size(), f); fclose(f); }
+  }
   nvrtcProgram prog;
   nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "bfa_kernel.cu", 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) return set_err(BFA_E_JIT, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
@@ -230,11 +242,6 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
 // generated source / of the program DAG and variant) so later processes
 // (other ranks, the next bench run) skip NVRTC and the search.  Only
 // preparation time depends on it, never results.  $BFA_JIT_CACHE=0 disables.
-uint64_t fnv64(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
-  const unsigned char* c = static_cast<const unsigned char*>(data);
-  for (size_t i = 0; i < n; i++) { h ^= c[i]; h *= 1099511628211ull; }
-  return h;
-}
 
 const std::string& cache_dir() {
   static std::string dir = [] {
@@ -307,6 +314,7 @@ struct Options {
   int multi_body = 0;            // 1: cofactor children of a piece as ONE multi-body launch (measured slower: occupancy of the largest child)
   int split_policy = 1;          // 0: split the heaviest piece; 1: split the piece whose best split saves the most work
   int queue_bodies = 0;          // > 0: decomposition leaves run as persistent work-queue kernels of <= this many bodies
+  int queue_chunk = 65536;       // work-queue chunk size (modelled thread-instructions)
 };
 
 struct JitEntry {
@@ -356,7 +364,7 @@ struct bfa_prog {
   };
   struct Queue {
     std::vector<QueueGroup> groups;
-    size_t bodies = 0;
+    size_t bodies = 0, unique = 0, units = 0;  // bodies, distinct body codes compiled, compile units
     uint64_t chunks = 0;
     double bodies_s = 0, nvrtc_s = 0;  // preparation: role searches + emission, NVRTC
     std::vector<uint8_t> queued;  // per piece
@@ -913,7 +921,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk;
   return k.str();
 }
 
@@ -1401,16 +1409,23 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
 }
 
 // The work-queue kernels over the pieces `rank` owns (host side, built once
-// per key): every eligible piece (non-constant, no further cofactor split, a
-// specialised whole-cube plan) becomes a noinline body with the FULL inner
-// loop (no piece has to fill the GPU alone, so none gives up loop-invariant
-// hoisting); the bodies, sorted by their per-iteration cell count (a proxy of
-// their register need), are cut into groups of <= queue_bodies bodies and
-// about equal estimated work (NVRTC time grows faster than linearly with a
-// module's size, and groups compile in parallel); within a group the heaviest bodies come first and every body is cut
-// into chunks of about equal work, 32 per SM per group.
+// per key).  Every eligible piece (non-constant, no further cofactor split,
+// <= 8000 LUTs) becomes a noinline device body with the FULL inner loop (no
+// piece has to fill the GPU alone, so none gives up loop-invariant hoisting)
+// and a per-warp sum.  The bodies, sorted by their per-iteration cell count
+// (a proxy of their register need), are cut into modules of <= queue_bodies
+// bodies (fewer when that leaves less than 4 modules per host core: NVRTC
+// compiles a module on one thread, in time growing faster than linearly with
+// its size) and about equal modelled work.  A module is one persistent
+// kernel: its bodies in order of decreasing work, each cut into chunks of
+// about queue_chunk modelled thread-instructions, which blocks pull with one
+// atomic.  Identical bodies of a module share one copy.  Modules are
+// compiled whole (not as separately linked objects: ptxas then allocates the
+// bodies' registers against the calling kernel, measured 1.65 vs 2.5 ms on
+// C5 with 32768 leaves), in parallel, cached on disk.
 int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::unique_ptr<bfa_prog>>& kids,
                  const std::vector<int>& owner, int rank, int sms, bfa_prog::Queue** out) {
+  (void)sms;
   {
     std::lock_guard<std::mutex> lk(holder->mu);
     auto it = holder->queues.find(key);
@@ -1433,7 +1448,8 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     bfa::KernelStats st;
     uint64_t O = 0;
     int m = 0, nv = 0;
-    double cost = 0, size = 0;
+    double cost = 0, size = 0, cost_o = 0;  // modelled thread-instructions: body, per outer iteration
+    uint64_t hash = 0;
   };
   std::vector<Body> B(elig.size());
   parallel_for(elig.size(), [&](size_t e) {
@@ -1448,20 +1464,26 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     spec.min_blocks = o.min_blocks;
     resolve_roles(q, &spec, b.nv);
     b.name = "bfa_body_" + std::to_string(i);
-    spec.body_name = b.name;
+    spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
     b.src = bfa::emit_kernel(q->parsed, spec, &b.st);
+    b.hash = fnv64(b.src.data(), b.src.size());
     b.O = (1ull << (b.nv - 5)) >> (s + t + b.m);
     const double inner = b.st.luts_inner + b.st.imads_inner + b.st.derived_inner;
     const double outer = b.st.luts_outer + b.st.imads_outer + b.st.derived_outer;
     b.size = inner;
-    b.cost = (double)b.O * (std::ldexp(inner + 2.0 * (1 << s) + 6.0, b.m) + outer + 12.0);
+    b.cost_o = std::ldexp(inner + 2.0 * (1 << s) + 6.0, b.m) + outer + 12.0;
+    b.cost = (double)b.O * b.cost_o;
   });
   bfa_prog::Queue Q;
   Q.queued.assign(kids.size(), 0);
   Q.bodies = elig.size();
   const auto t1 = std::chrono::steady_clock::now();
   Q.bodies_s = std::chrono::duration<double>(t1 - t0).count();
-  const int G = (int)((elig.size() + std::max(1, o.queue_bodies) - 1) / std::max(1, o.queue_bodies));
+  // modules: <= `per` bodies, about equal modelled work, over the size order
+  const size_t cores = std::max(1u, std::thread::hardware_concurrency());
+  const int per = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(1, o.queue_bodies),
+                                                            std::max<size_t>(16, (elig.size() + 4 * cores - 1) / (4 * cores))));
+  const int G = (int)((elig.size() + per - 1) / per);
   std::vector<size_t> order(elig.size());
   for (size_t e = 0; e < order.size(); e++) order[e] = e;
   std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return B[x].size > B[y].size; });
@@ -1471,16 +1493,16 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
   {
     double run = 0;
     int g = 0;
-    for (size_t r = 0; r < order.size(); r++) {
+    for (size_t e : order) {
       const int gw = (int)std::min<double>(G - 1, std::floor(run / std::max(total, 1e-30) * G));
-      if ((gw > g || (int)groups[g].size() >= o.queue_bodies) && g + 1 < G) g++;
-      groups[g].push_back(order[r]);
-      run += B[order[r]].cost;
+      if ((gw > g || (int)groups[g].size() >= per) && g + 1 < G) g++;
+      groups[g].push_back(e);
+      run += B[e].cost;
     }
-    // the work boundaries can leave more than queue_bodies in the last group
-    while (!groups.empty() && (int)groups.back().size() > o.queue_bodies) {
-      std::vector<size_t> tail(groups.back().begin() + o.queue_bodies, groups.back().end());
-      groups.back().resize(o.queue_bodies);
+    // the work boundaries can leave more than `per` bodies in the last module
+    while (!groups.empty() && (int)groups.back().size() > per) {
+      std::vector<size_t> tail(groups.back().begin() + per, groups.back().end());
+      groups.back().resize(per);
       groups.push_back(std::move(tail));
     }
   }
@@ -1488,19 +1510,32 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
   for (auto& gm : groups) {
     if (gm.empty()) continue;
     std::stable_sort(gm.begin(), gm.end(), [&](size_t x, size_t y) { return B[x].cost > B[y].cost; });
-    double gcost = 0;
-    for (size_t e : gm) gcost += B[e].cost;
-    const double target = 32.0 * sms;
     std::vector<std::string> bsrc, bname;
     std::vector<uint64_t> O;
     std::vector<uint32_t> ch;
     bfa_prog::QueueGroup qg;
+    std::map<uint64_t, std::string> seen;  // body hash -> name of its copy in this module
     for (size_t e : gm) {
       const Body& b = B[e];
-      const double want = std::llround(target * b.cost / std::max(gcost, 1e-30));
-      const uint32_t c = (uint32_t)std::max<double>(1.0, std::min<double>((double)b.O, want));
-      bsrc.push_back(b.src);
-      bname.push_back(b.name);
+      // chunks of ~queue_chunk modelled thread-instructions (65536: ~0.1-0.2
+      // ms of a block): long enough to amortise the dispatch and the body's
+      // instruction-cache warm-up (C5, 16384 leaves: 2048 -> 3.25 ms, 8192 ->
+      // 2.68, 32768 -> 2.28, 131072 -> 2.26, 524288 -> 2.35: one chunk per body)
+      const double pc = std::max(1.0, std::floor((double)o.queue_chunk / std::max(b.cost_o, 1.0)));
+      const uint32_t c = (uint32_t)std::max<double>(1.0, std::ceil((double)b.O / pc));
+      auto sn = seen.find(b.hash);
+      if (sn == seen.end()) {
+        std::string src = b.src;
+        const size_t at = src.find("bfa_body_X");
+        if (at != std::string::npos) src.replace(at, 10, b.name);
+        bsrc.push_back(std::move(src));
+        bname.push_back(b.name);
+        seen.emplace(b.hash, b.name);
+        Q.unique++;
+      } else {
+        bsrc.emplace_back();
+        bname.push_back(sn->second);
+      }
       O.push_back(b.O);
       ch.push_back(c);
       qg.members.push_back(elig[e]);
@@ -1523,12 +1558,16 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
   for (int r : rcs)
     if (r) return r;
   Q.nvrtc_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t1).count();
+  Q.units = Q.groups.size();
   std::lock_guard<std::mutex> lk(holder->mu);
   auto it = holder->queues.find(key);
   if (it == holder->queues.end()) it = holder->queues.emplace(key, std::move(Q)).first;
   *out = &it->second;
   return BFA_OK;
 }
+
+int prepare_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int sms,
+                   bfa_prog* holder, const std::string& qkey, bfa_prog::Queue** q_out);
 
 thread_local std::string g_queue_report;  // the last count_pieces' work-queue summary (JSON object or empty)
 
@@ -1539,24 +1578,11 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
   cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
   if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
   bfa_prog::Queue* Q = nullptr;
-  if (holder && holder->opt.queue_bodies > 0) {
-    int rc = ensure_queue(holder, qkey, kids, owner, rank, sms, &Q);
+  {
+    int rc = prepare_pieces(kids, owner, rank, sms, holder, qkey, &Q);
     if (rc) return rc;
   }
   auto queued = [&](size_t i) { return Q && Q->queued[i]; };
-  {  // compile the owned pieces' kernels in parallel (pieces that split
-     // further into cofactor kernels prepare their own children)
-    std::vector<size_t> todo;
-    for (size_t i = 0; i < kids.size(); i++)
-      if (owner[i] == rank && kids[i]->info.const_value != 0 && !queued(i)) todo.push_back(i);
-    std::vector<int> rcs(todo.size(), 0);
-    parallel_for(todo.size(), [&](size_t e) {
-      const size_t i = todo[e];
-      rcs[e] = kids[i]->opt.kernel_cofactor_bits == 0 ? prepare_count(kids[i].get(), kids[i]->piece_nv, sms)
-                                                      : prepare_split(kids[i].get(), kids[i]->piece_nv, sms);
-    });
-    for (int r : rcs) if (r) return r;
-  }
   // every piece adds into count_dev (a piece that splits into its own
   // cofactor kernels accumulates too); pieces run on forked side streams
   int kernels = 0;
@@ -1578,15 +1604,14 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
       Q->ctr[dev] = ctr;
     }
     const int T = 1 << holder->opt.thread_bits;
-    std::ostringstream qr;
-    qr << "{\"modules\": " << Q->groups.size() << ", \"bodies\": " << Q->bodies << ", \"chunks\": " << Q->chunks
-       << ", \"bodies_s\": " << Q->bodies_s << ", \"nvrtc_s\": " << Q->nvrtc_s << "}";
-    g_queue_report = qr.str();
+
+    std::string regs;
     for (size_t g = 0; g < Q->groups.size(); g++) {
       auto& qg = Q->groups[g];
       JitEntry* je = nullptr;
       CUfunction fn;
       if ((rc = get_kernel_src(holder, qg.src_key, "", holder->opt.thread_bits, dev, &je, &fn))) return rc;
+      regs += (g ? ", " : "") + std::to_string(je->regs);
       unsigned grid = (unsigned)std::min<uint64_t>(qg.chunks, (uint64_t)sms * je->occupancy[dev]);
       uint64_t* cnt = count_dev;
       uint32_t* c = ctr + g;
@@ -1596,6 +1621,11 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
       im += qg.im;
       kernels++;
     }
+    std::ostringstream qr;
+    qr << "{\"modules\": " << Q->groups.size() << ", \"bodies\": " << Q->bodies << ", \"unique\": " << Q->unique
+       << ", \"units\": " << Q->units << ", \"chunks\": " << Q->chunks << ", \"regs\": [" << regs
+       << "], \"bodies_s\": " << Q->bodies_s << ", \"nvrtc_s\": " << Q->nvrtc_s << "}";
+    g_queue_report = qr.str();
   }
   for (size_t i = 0; i < kids.size(); i++) {
     if (owner[i] != rank || queued(i)) continue;
@@ -1628,34 +1658,66 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
 // Single-device count of an aligned sub-cube through a Shannon
 // decomposition into split_pieces pieces (each with its own kernel-level
 // cofactoring); pieces are prepared once and cached.
-int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st) {
-  int dev;
-  DevInfo di;
-  int rc = current_device(&dev, &di);
-  if (rc) return rc;
+// The cached Shannon decomposition of the aligned 2^k sub-cube at mu_lo.
+std::vector<std::unique_ptr<bfa_prog>>* get_decomposition(const bfa_prog* p, int n, uint64_t mu_lo, int k,
+                                                          std::string* key_out) {
   bfa_prog* mp = const_cast<bfa_prog*>(p);
   const uint64_t top_mask = (k >= 64) ? 0 : (~0ull << k) & ((n >= 64) ? ~0ull : ((1ull << n) - 1));
   const uint64_t top_vals = mu_lo & top_mask;
   const std::string key = "split." + std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) +
                           "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits) +
                           "." + std::to_string(p->opt.split_policy);
-  std::vector<std::unique_ptr<bfa_prog>>* kids = nullptr;
+  *key_out = key;
   {
     std::lock_guard<std::mutex> lk(mp->mu);
     auto it = mp->cofactors.find(key);
-    if (it != mp->cofactors.end()) kids = &it->second;
+    if (it != mp->cofactors.end()) return &it->second;
   }
-  if (!kids) {
-    const auto t0 = std::chrono::steady_clock::now();
-    std::vector<std::unique_ptr<bfa_prog>> made =
-        decompose(p, bfa::assume(p->parsed, n, top_mask, top_vals, nullptr), k, p->opt.split_pieces);
-    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    std::lock_guard<std::mutex> lk(mp->mu);
-    auto it = mp->cofactors.find(key);
-    if (it == mp->cofactors.end()) it = mp->cofactors.emplace(key, std::move(made)).first;
-    kids = &it->second;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::unique_ptr<bfa_prog>> made =
+      decompose(p, bfa::assume(p->parsed, n, top_mask, top_vals, nullptr), k, p->opt.split_pieces);
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::lock_guard<std::mutex> lk(mp->mu);
+  auto it = mp->cofactors.find(key);
+  if (it == mp->cofactors.end()) {
+    it = mp->cofactors.emplace(key, std::move(made)).first;
     mp->decompose_s[key] = secs;
   }
+  return &it->second;
+}
+
+// Host-side preparation of the owned pieces of a decomposition: the
+// work-queue modules (queue_bodies > 0) and every other piece's kernels.
+int prepare_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector<int>& owner, int rank, int sms,
+                   bfa_prog* holder, const std::string& qkey, bfa_prog::Queue** q_out) {
+  bfa_prog::Queue* Q = nullptr;
+  if (holder && holder->opt.queue_bodies > 0) {
+    int rc = ensure_queue(holder, qkey, kids, owner, rank, sms, &Q);
+    if (rc) return rc;
+  }
+  if (q_out) *q_out = Q;
+  std::vector<size_t> todo;
+  for (size_t i = 0; i < kids.size(); i++)
+    if (owner[i] == rank && kids[i]->info.const_value != 0 && !(Q && Q->queued[i])) todo.push_back(i);
+  std::vector<int> rcs(todo.size(), 0);
+  parallel_for(todo.size(), [&](size_t e) {  // pieces that split further prepare their own children
+    const size_t i = todo[e];
+    rcs[e] = kids[i]->opt.kernel_cofactor_bits == 0 ? prepare_count(kids[i].get(), kids[i]->piece_nv, sms)
+                                                    : prepare_split(kids[i].get(), kids[i]->piece_nv, sms);
+  });
+  for (int r : rcs)
+    if (r) return r;
+  return BFA_OK;
+}
+
+int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st) {
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  bfa_prog* mp = const_cast<bfa_prog*>(p);
+  std::string key;
+  std::vector<std::unique_ptr<bfa_prog>>* kids = get_decomposition(p, n, mu_lo, k, &key);
   std::vector<int> owner(kids->size(), 0);
   int kernels = 0, zero = 0;
   uint64_t zero_vals = 0;
@@ -1855,8 +1917,49 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "multi_body") { if (v < 0 || v > 1) return bad(); p->opt.multi_body = (int)v; }
   else if (k == "split_policy") { if (v < 0 || v > 1) return bad(); p->opt.split_policy = (int)v; }
   else if (k == "queue_bodies") { if (v < 0 || v > 8192) return bad(); p->opt.queue_bodies = (int)v; }
+  else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
+}
+
+int bfa_prepare(const bfa_prog* p, int n, int sms) {
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  if (p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "program uses x%d >= n", p->info.max_var_id);
+  if (sms <= 0) {
+    int count = 0;
+    sms = 148;  // B200
+    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
+      int dev;
+      DevInfo di;
+      if (current_device(&dev, &di) == BFA_OK) sms = di.sms;
+    } else {
+      cudaGetLastError();
+    }
+  }
+  const Options& o = p->opt;
+  const bool plain = !o.force_generic && !o.engine && !o.segment_cells && p->info.luts <= 8000;
+  if (plain && o.split_pieces > 1 && n >= 30) {
+    std::string key;
+    std::vector<std::unique_ptr<bfa_prog>>* kids = get_decomposition(p, n, 0, n, &key);
+    std::vector<int> owner(kids->size(), 0);
+    bfa_prog::Queue* Q = nullptr;
+    int rc = prepare_pieces(*kids, owner, 0, sms, const_cast<bfa_prog*>(p), "q." + key, &Q);
+    if (rc) return rc;
+    bfa_prog* mp = const_cast<bfa_prog*>(p);
+    std::ostringstream js;
+    std::lock_guard<std::mutex> lk(mp->mu);
+    js << "{\"variant\": \"prepare\", \"pieces\": " << kids->size() << ", \"decompose_s\": " << mp->decompose_s[key];
+    if (Q)
+      js << ", \"queue\": {\"modules\": " << Q->groups.size() << ", \"bodies\": " << Q->bodies << ", \"unique\": "
+         << Q->unique << ", \"chunks\": "
+         << Q->chunks << ", \"bodies_s\": " << Q->bodies_s << ", \"nvrtc_s\": " << Q->nvrtc_s << "}";
+    js << "}";
+    g_last_launch = js.str();
+    return BFA_OK;
+  }
+  if (plain && o.kernel_cofactor_bits > 0 && n >= 24 + o.kernel_cofactor_bits) return prepare_split(p, n, sms);
+  return prepare_count(p, n, sms);
 }
 
 int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* count_dev, void* stream) {
@@ -2002,8 +2105,8 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   // caller will count: 2^k_free valuations when that takes <= ~2 s, else the
   // probe).  Stage A: kernel-level cofactoring, 2^j cofactor kernels.  Stage
   // Q: a Shannon decomposition into split_pieces leaves run as work-queue
-  // kernels of <= 512 bodies, 4096 and 16384 leaves (32768 when 16384 won and
-  // prepared in under a minute); only when the whole count takes > 1 ms.
+  // kernels of <= 512 bodies, 16384 leaves (then 32768 when 16384 won and
+  // prepared in under 150 s); only when the whole count takes > 1 ms.
   struct Trial { int sp, j, qb; float ms; double prep_s; };
   std::vector<Trial> kcof;
   if (best >= 0 && k_free >= 28) {
@@ -2042,9 +2145,8 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     for (int jj : {0, 4})
       if ((rc = trial(0, jj, 0))) break;
     if (!rc && bestt.ms > 1.0f) {
-      for (int sp : {4096, 16384})
-        if ((rc = trial(sp, 0, 512))) break;
-      if (!rc && bestt.sp == 16384 && kcof.back().prep_s < 60.0) rc = trial(32768, 0, 512);
+      rc = trial(16384, 0, 512);
+      if (!rc && bestt.sp == 16384 && kcof.back().prep_s < 150.0) rc = trial(32768, 0, 512);
     }
     if (rc) p->opt = cands[best].o;
     p->opt.kernel_cofactor_bits = bestt.j;

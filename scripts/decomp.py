@@ -41,4 +41,5 @@ for spec in sys.argv[3:]:
     floor = max(l3 / 18.6e12, (l3 + im) / 35.2e12) * 1e3   # ALU-pipe / issue bound, ms
     print(json.dumps({"sp": sp, "j": j, "ms": round(s.elapsed_time(e) / 5, 3), "ok": c == ref, "prep_s": round(prep, 1),
                       "count": c, "decided": ll.get("valuations_decided"), "kernels": ll.get("kernels"),
-                      "cells_lop3": l3, "cells_imad": im, "alu_floor_ms": round(floor, 3)}), flush=True)
+                      "cells_lop3": l3, "cells_imad": im, "alu_floor_ms": round(floor, 3),
+                      "decompose_s": ll.get("decompose_s"), "queue": ll.get("queue")}), flush=True)

@@ -1,0 +1,4 @@
+for S in 4 1 2 8; do
+B="{\"slot_bits\": 5, \"inner_bits\": 4, \"imad_cost_pct\": 50, \"dual_pipe\": 1, \"queue_bodies\": 512, \"streams\": $S}"
+echo "streams $S"; timeout 1200 python scripts/decomp.py c5 "$B" 32768,0 2>&1 | grep -v Traceback | tail -1 | cut -c1-400
+done
