@@ -1447,7 +1447,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     std::string name, src;
     bfa::KernelStats st;
     uint64_t O = 0;
-    int m = 0, nv = 0;
+    int m = 0, nv = 0, s = 0;
     double cost = 0, size = 0, cost_o = 0;  // modelled thread-instructions: body, per outer iteration
     uint64_t hash = 0;
   };
@@ -1457,9 +1457,10 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     bfa_prog* q = kids[i].get();
     Body& b = B[e];
     b.nv = q->piece_nv;
-    b.m = std::min(o.inner_bits, b.nv - 5 - s - t);
+    b.s = s;
+    b.m = std::min(o.inner_bits, b.nv - 5 - b.s - t);
     bfa::KernelSpec spec;
-    spec.mode = bfa::KM_COUNT; spec.generic = false; spec.slot_bits = s; spec.thread_bits = t;
+    spec.mode = bfa::KM_COUNT; spec.generic = false; spec.slot_bits = b.s; spec.thread_bits = t;
     spec.inner_bits = b.m; spec.dual_pipe = o.dual_pipe; spec.imad_cost_pct = o.imad_cost_pct;
     spec.min_blocks = o.min_blocks;
     resolve_roles(q, &spec, b.nv);
@@ -1467,11 +1468,11 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
     b.src = bfa::emit_kernel(q->parsed, spec, &b.st);
     b.hash = fnv64(b.src.data(), b.src.size());
-    b.O = (1ull << (b.nv - 5)) >> (s + t + b.m);
+    b.O = (1ull << (b.nv - 5)) >> (b.s + t + b.m);
     const double inner = b.st.luts_inner + b.st.imads_inner + b.st.derived_inner;
     const double outer = b.st.luts_outer + b.st.imads_outer + b.st.derived_outer;
     b.size = inner;
-    b.cost_o = std::ldexp(inner + 2.0 * (1 << s) + 6.0, b.m) + outer + 12.0;
+    b.cost_o = std::ldexp(inner + 2.0 * (1 << b.s) + 6.0, b.m) + outer + 12.0;
     b.cost = (double)b.O * b.cost_o;
   });
   bfa_prog::Queue Q;
@@ -1541,7 +1542,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
       qg.members.push_back(elig[e]);
       qg.chunks += c;
       Q.queued[elig[e]] = 1;
-      const double S = 1 << s, it = std::ldexp(1.0, b.m), words = std::ldexp(1.0, b.nv - 5);
+      const double S = 1 << b.s, it = std::ldexp(1.0, b.m), words = std::ldexp(1.0, b.nv - 5);
       qg.l3 += words * (b.st.luts_inner / S + b.st.luts_outer / (S * it));
       qg.im += words * ((b.st.imads_inner + b.st.derived_inner) / S +
                         (b.st.imads_outer + b.st.derived_outer) / (S * it));

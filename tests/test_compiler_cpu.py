@@ -192,3 +192,22 @@ def test_assume_to_constant():
     assert q.info["const_value"] == 1 and nf == 4 and ids == [1, 2, 3, 4]
     q, nf, _ = bfa.Program("x63 & x1").assume(64, {63: 0})
     assert q.info["const_value"] == 0 and nf == 63
+
+
+def test_prepare_host_only():
+    """bfa_prepare runs every host-side step of a count without a GPU: the
+    Shannon decomposition, role searches, emission and NVRTC of the
+    work-queue modules (sm_100a) -- and reports them; bad n is rejected."""
+    text, n, _ = W.config("c5")
+    p = bfa.Program(text).set_option("split_pieces", 48).set_option("queue_bodies", 8)
+    p.set_option("slot_bits", 3)
+    p.prepare(n, 148)
+    ll = bfa.last_launch()
+    assert ll["variant"] == "prepare" and ll["pieces"] >= 48
+    q = ll["queue"]
+    assert 0 < q["unique"] <= q["bodies"] <= 48 and q["modules"] >= -(-q["bodies"] // 8)
+    assert q["chunks"] >= q["bodies"]
+    p.prepare(n, 148)                     # cached: a second call is free
+    with pytest.raises(bfa.BfaError):
+        p.prepare(40)                     # the program uses x41
+    bfa.Program(W.posets(4)).prepare(16)  # plain kernel path
