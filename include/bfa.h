@@ -129,6 +129,8 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   sets it)
  *   "queue_chunk"   work-queue chunk size in modelled thread-instructions
  *                   (default 65536)
+ *   "queue_inner"   inner-loop bits of work-queue bodies (default 2; -1:
+ *                   inner_bits)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 

@@ -1,0 +1,5 @@
+for C in 16384 262144; do
+B="{\"slot_bits\": 5, \"inner_bits\": 4, \"imad_cost_pct\": 50, \"dual_pipe\": 1, \"queue_bodies\": 512, \"queue_chunk\": $C}"
+echo "chunk $C"; timeout 1500 python scripts/decomp.py c5 "$B" 32768,0 2>&1 | grep -v Traceback | tail -1 | python -c "
+import json,sys; d=json.loads(sys.stdin.read()); q=d['queue']; print(d['ms'], d['prep_s'], q['chunks'])"
+done
