@@ -131,6 +131,9 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   (default 65536)
  *   "queue_inner"   inner-loop bits of work-queue bodies (default 2; -1:
  *                   inner_bits)
+ *   "queue_support" 1: a work-queue body enumerates only the variables its
+ *                   leaf depends on (and enough others for the body layout);
+ *                   its count is scaled by 2^(dropped) (default 0)
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 

@@ -1119,7 +1119,9 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     os << "    }\n"
        << "    acc += acc32;\n"
        << "  }\n";
-    if (want_count) os << (as_body ? "  bfa_warp_sum(acc, count);\n" : "  bfa_block_sum(acc, count);\n");
+    const std::string acc_expr = spec.count_shift ? "acc << " + std::to_string(spec.count_shift) : "acc";
+    if (want_count)
+      os << (as_body ? "  bfa_warp_sum(" : "  bfa_block_sum(") << acc_expr << ", count);\n";
     os << "}\n";
     st.words_per_iter = (uint32_t)S;
   }

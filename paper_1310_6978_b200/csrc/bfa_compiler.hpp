@@ -138,6 +138,8 @@ struct KernelSpec {
                               // word/valuation index (empty = identity)
   std::string body_name;      // non-empty: emit the specialised kernel as a
                               // __device__ __noinline__ body of a multi-body kernel
+  int count_shift = 0;        // count mode: the count is scaled by 2^count_shift
+                              // (support reduction: variables outside the support)
 };
 
 struct KernelStats {

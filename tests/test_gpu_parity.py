@@ -340,8 +340,13 @@ def test_work_queue_kernels():
     a = int(p.count_range(n, lo, lo + (1 << 32)).item())
     assert a == ref
     assert a + int(pc.count_range(n, lo, lo + (1 << 32)).item()) == 1 << 32
-    p = bfa.Program(text).set_option("split_pieces", 256).set_option("queue_bodies", 32)
     full = bfa.Program(text).count(n)
+    for sup in (0, 1):                   # support reduction: counts scaled by 2^(dropped variables)
+        p = bfa.Program(text).set_option("split_pieces", 1024).set_option("queue_bodies", 64)
+        p.set_option("queue_support", sup)
+        assert p.count(n) == full
+        assert (bfa.last_launch()["queue"]["support_reduced"] > 0) == bool(sup)
+    p = bfa.Program(text).set_option("split_pieces", 256).set_option("queue_bodies", 32)
     for world in (2, 4):
         shares = [int(p.count_shard(n, r, world).item()) for r in range(world)]
         assert sum(shares) == full
