@@ -29,6 +29,7 @@
 #include <atomic>
 #include <chrono>
 #include <mutex>
+#include <unordered_map>
 #include <set>
 #include <queue>
 #include <sstream>
@@ -316,6 +317,7 @@ struct Options {
   int queue_bodies = 0;          // > 0: decomposition leaves run as persistent work-queue kernels of <= this many bodies
   int queue_chunk = 65536;       // work-queue chunk size (modelled thread-instructions)
   int queue_inner = 2;           // inner-loop bits of work-queue bodies (-1: inner_bits)
+  int split_merge = 0;           // > 0: merge sibling leaves of <= this many gates back into their parent
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -925,7 +927,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge;
   return k.str();
 }
 
@@ -1190,6 +1192,7 @@ void parallel_for(size_t n, F f) {
 struct Piece {
   std::unique_ptr<bfa_prog> prog;
   int nv = 0;
+  int id = 0;           // unique per node of the split tree
   uint64_t work = 0;
   int split_v = -1;     // best single split variable (-1: not splittable)
   uint64_t gain = 0;    // work saved by splitting on split_v
@@ -1250,14 +1253,17 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
   };
   if (splittable(0)) heap.push(0);
   int live = pieces[0].work > 0;
-  // pieces are split in batches (the top of the heap, at most one per host
-  // core and no more than the target still needs), the splits of a batch in
-  // parallel; the batches depend only on the heap, so every rank gets the same
-  // decomposition
-  const size_t cores = std::max(1u, std::thread::hardware_concurrency());
+  // pieces are split in batches (the top of the heap, at most 16 and no more
+  // than the target still needs), the splits of a batch in parallel; the
+  // batches depend only on the heap, so every rank (and machine) gets the
+  // same decomposition
+  const size_t kBatch = 16;
+  struct Inner { std::unique_ptr<bfa_prog> prog; int nv; uint64_t work; int id, c0, c1; };
+  std::vector<Inner> inner;  // split nodes, in split order
+  int next_id = 1;
   while (live < target && !heap.empty()) {
     std::vector<size_t> batch;
-    while (!heap.empty() && batch.size() < cores && live - (int)batch.size() + 2 * (int)(batch.size() + 1) <= target + 1) {
+    while (!heap.empty() && batch.size() < kBatch && live - (int)batch.size() + 2 * (int)(batch.size() + 1) <= target + 1) {
       batch.push_back(heap.top());
       heap.pop();
     }
@@ -1287,12 +1293,46 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
     });
     for (size_t e = 0; e < batch.size(); e++) {
       const size_t h = batch[e];
-      for (int b = 0; b < 2; b++) live += kid[2 * e + b].work > 0;
+      for (int b = 0; b < 2; b++) {
+        live += kid[2 * e + b].work > 0;
+        kid[2 * e + b].id = next_id++;
+      }
+      inner.push_back({std::move(big[e].prog), big[e].nv, big[e].work, big[e].id, kid[2 * e].id, kid[2 * e + 1].id});
       pieces[h] = std::move(kid[2 * e]);        // cofactor 0 takes the parent's slot,
       pieces.push_back(std::move(kid[2 * e + 1]));  // cofactor 1 goes to the end
       if (splittable(h)) heap.push(h);
       if (splittable(pieces.size() - 1)) heap.push(pieces.size() - 1);
     }
+  }
+  // merge light sibling leaves back into their parent, bottom-up: two
+  // non-constant leaves of <= split_merge gates each cost more as two bodies
+  // (each fetched and dispatched for very little work) than their parent as one
+  if (p->opt.split_merge > 0) {
+    std::unordered_map<int, size_t> slot_of;
+    for (size_t i = 0; i < pieces.size(); i++) slot_of[pieces[i].id] = i;
+    for (size_t k = inner.size(); k-- > 0;) {
+      Inner& in = inner[k];
+      auto a = slot_of.find(in.c0), b = slot_of.find(in.c1);
+      if (a == slot_of.end() || b == slot_of.end()) continue;
+      Piece& A = pieces[a->second];
+      Piece& B = pieces[b->second];
+      if (A.work == 0 || B.work == 0) continue;  // a constant-0 half costs nothing
+      if ((int)A.prog->info.gates > p->opt.split_merge || (int)B.prog->info.gates > p->opt.split_merge) continue;
+      const size_t sa = a->second, sb = b->second;
+      slot_of.erase(a);
+      slot_of.erase(in.c1);
+      pieces[sb].prog.reset();
+      pieces[sb].work = 0;
+      pieces[sa].prog = std::move(in.prog);
+      pieces[sa].nv = in.nv;
+      pieces[sa].work = in.work;
+      pieces[sa].id = in.id;
+      slot_of[in.id] = sa;
+    }
+    std::vector<Piece> kept;
+    for (auto& x : pieces)
+      if (x.prog) kept.push_back(std::move(x));
+    pieces.swap(kept);
   }
   std::vector<std::unique_ptr<bfa_prog>> made;
   for (auto& x : pieces) {
@@ -1722,7 +1762,7 @@ std::vector<std::unique_ptr<bfa_prog>>* get_decomposition(const bfa_prog* p, int
   const uint64_t top_vals = mu_lo & top_mask;
   const std::string key = "split." + std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) +
                           "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits) +
-                          "." + std::to_string(p->opt.split_policy);
+                          "." + std::to_string(p->opt.split_policy) + "." + std::to_string(p->opt.split_merge);
   *key_out = key;
   {
     std::lock_guard<std::mutex> lk(mp->mu);
@@ -1973,6 +2013,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "multi_body") { if (v < 0 || v > 1) return bad(); p->opt.multi_body = (int)v; }
   else if (k == "split_policy") { if (v < 0 || v > 1) return bad(); p->opt.split_policy = (int)v; }
   else if (k == "queue_bodies") { if (v < 0 || v > 8192) return bad(); p->opt.queue_bodies = (int)v; }
+  else if (k == "split_merge") { if (v < 0 || v > 100000) return bad(); p->opt.split_merge = (int)v; }
   else if (k == "queue_support") { if (v < 0 || v > 1) return bad(); p->opt.queue_support = (int)v; }
   else if (k == "queue_inner") { if (v < -1 || v > 8) return bad(); p->opt.queue_inner = (int)v; }
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
