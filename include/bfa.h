@@ -131,6 +131,9 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   (default 65536)
  *   "queue_inner"   inner-loop bits of work-queue bodies (default 2; -1:
  *                   inner_bits)
+ *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
+ *                   leaves of <= this many gates each back into their parent
+ *                   (default 0)
  *   "queue_support" 1: a work-queue body enumerates only the variables its
  *                   leaf depends on (and enough others for the body layout);
  *                   its count is scaled by 2^(dropped) (default 0)

@@ -211,3 +211,23 @@ def test_prepare_host_only():
     with pytest.raises(bfa.BfaError):
         p.prepare(40)                     # the program uses x41
     bfa.Program(W.posets(4)).prepare(16)  # plain kernel path
+
+
+def test_decomposition_tiles_the_cube():
+    """The Shannon decomposition (host only) tiles the 2^n cube for both split
+    policies and with the light-sibling merge: sum of 2^vars over the pieces
+    is 2^n, the requested number of non-constant pieces is reached (merge
+    only removes pieces), and the plan is reproducible."""
+    text, n, _ = W.config("c5")
+    sizes = {}
+    for policy, merge in ((0, 0), (1, 0), (1, 16)):
+        p = bfa.Program(text).set_option("split_pieces", 512).set_option("split_policy", policy)
+        p.set_option("split_merge", merge)
+        plan = p.shard_plan(n, 1)
+        assert sum(1 << nv for _, nv, _ in plan) == 1 << n
+        live = sum(1 for _, _, w in plan if w)
+        sizes[(policy, merge)] = live
+        assert plan == bfa.Program(text).set_option("split_pieces", 512).set_option(
+            "split_policy", policy).set_option("split_merge", merge).shard_plan(n, 1)
+    assert sizes[(0, 0)] >= 512 and sizes[(1, 0)] >= 512
+    assert sizes[(1, 16)] <= sizes[(1, 0)]
