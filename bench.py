@@ -11,10 +11,15 @@ random 1000-gate Boolean DAG over n = 42 variables, 2^42 valuations per step.
     python bench.py --impl reference ...                   (the CPU oracle arm)
 
 A step = one full pass of the hot path over the step's batch: every rank
-counts its cofactor range [r 2^(n-p), (r+1) 2^(n-p)) with the JIT'd
-register-mode kernel (generators synthesised in registers, straight-line
-LOP3 body, fused popcount + block/grid reduction), then ONE NCCL all-reduce
-of the 8-byte count (P > 1).  Timing: W untimed warm-up steps; L2 flushed
+counts its share of the 2^n cube with the JIT'd register-mode kernels
+(generators synthesised in registers, straight-line LOP3/IMAD bodies, fused
+popcount + reduction) -- with the autotuned configuration, the leaves of a
+Shannon decomposition (its pieces balanced over the ranks by
+bfa_count_shard) run as persistent work-queue kernels replayed from one CUDA
+graph -- then ONE NCCL all-reduce of the 8-byte count (P > 1).  Leaves the
+Reduction proves identically 0 are decided at preparation time and reported
+(decided_at_compile_time); preparation (autotune + JIT) is outside the timed
+region and reported as jit_prep_s.  Timing: W untimed warm-up steps; L2 flushed
 (256 MiB write) before every timed step; CUDA events on the launching stream
 around each step; barrier + synchronize on both sides; max over ranks.
 Prints one JSON line on rank 0.
