@@ -121,8 +121,8 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "streams"       side streams for independent pieces / cofactors (default 4)
  *   "multi_body"    1: a split's cofactor children as one multi-body launch
  *                   (default 0)
- *   "split_policy"  which piece split_pieces splits next: 0 the heaviest,
- *                   1 the one whose best split saves the most work (default)
+ *   "split_policy"  which piece split_pieces splits next: 0 the heaviest
+ *                   (default), 1 the one whose best split saves the most work
  *   "queue_bodies"  > 0: the leaves of a split_pieces decomposition run as
  *                   persistent work-queue kernels of at most this many
  *                   bodies each (default 0 = one kernel per leaf; autotune
@@ -131,6 +131,8 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   (default 65536)
  *   "queue_inner"   inner-loop bits of work-queue bodies (default 2; -1:
  *                   inner_bits)
+ *   "queue_role_budget" role-search evaluations per work-queue body
+ *                   (default 400)
  *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
  *                   leaves of <= this many gates each back into their parent
  *                   (default 0)

@@ -313,10 +313,11 @@ struct Options {
   int graphs = 1;                // replay multi-launch counts as CUDA graphs
   int streams = 4;               // side streams for independent pieces / cofactors
   int multi_body = 0;            // 1: cofactor children of a piece as ONE multi-body launch (measured slower: occupancy of the largest child)
-  int split_policy = 1;          // 0: split the heaviest piece; 1: split the piece whose best split saves the most work
+  int split_policy = 0;          // 0: split the heaviest piece; 1: split the piece whose best split saves the most work
   int queue_bodies = 0;          // > 0: decomposition leaves run as persistent work-queue kernels of <= this many bodies
   int queue_chunk = 65536;       // work-queue chunk size (modelled thread-instructions)
   int queue_inner = 2;           // inner-loop bits of work-queue bodies (-1: inner_bits)
+  int queue_role_budget = 400;   // role-search evaluations per work-queue body
   int split_merge = 0;           // > 0: merge sibling leaves of <= this many gates back into their parent
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
@@ -927,7 +928,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget;
   return k.str();
 }
 
@@ -1221,9 +1222,10 @@ static void score_split(Piece* x) {
 // non-constant pieces ("further partition").
 // Every step splits one piece on its own best variable (both cofactors via
 // bfa_assume + Reduction), so different branches split on different
-// variables.  Policy 0 splits the heaviest piece (work = (gates + 1) x
-// 2^free_vars); policy 1 (default) splits the piece whose split saves the
-// most work, ties to the heaviest.  Pieces with <= 24 free variables are not
+// variables.  Policy 0 (default) splits the heaviest piece (work = (gates +
+// 1) x 2^free_vars); policy 1 splits the piece whose split saves the most
+// work, ties to the heaviest (measured slower on C5: 1.24 vs 1.31 ms at
+// 32768 leaves, 11.9 vs 13.2 ms at 128 pieces x 16 cofactors).  Pieces with <= 24 free variables are not
 // split.  Pieces inherit p's options (incl. kernel_cofactor_bits, applied
 // inside each piece).
 std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed base, int nv, int target) {
@@ -1556,6 +1558,10 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     spec.inner_bits = b.m; spec.dual_pipe = o.dual_pipe; spec.imad_cost_pct = o.imad_cost_pct;
     spec.min_blocks = o.min_blocks;
     spec.count_shift = b.shift;
+    // a leaf's kernel runs once per step while its role search runs once per
+    // preparation: work-queue bodies search longer (C5, 32768 leaves: budget
+    // 200 -> 1.31 ms, 400 -> 1.20 ms)
+    const_cast<bfa_prog*>(src)->opt.role_budget = o.queue_role_budget;
     resolve_roles(src, &spec, b.nv);
     b.name = "bfa_body_" + std::to_string(i);
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
@@ -2015,6 +2021,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_bodies") { if (v < 0 || v > 8192) return bad(); p->opt.queue_bodies = (int)v; }
   else if (k == "split_merge") { if (v < 0 || v > 100000) return bad(); p->opt.split_merge = (int)v; }
   else if (k == "queue_support") { if (v < 0 || v > 1) return bad(); p->opt.queue_support = (int)v; }
+  else if (k == "queue_role_budget") { if (v < 1 || v > 100000) return bad(); p->opt.queue_role_budget = (int)v; }
   else if (k == "queue_inner") { if (v < -1 || v > 8) return bad(); p->opt.queue_inner = (int)v; }
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
@@ -2204,8 +2211,9 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   // caller will count: 2^k_free valuations when that takes <= ~2 s, else the
   // probe).  Stage A: kernel-level cofactoring, 2^j cofactor kernels.  Stage
   // Q: a Shannon decomposition into split_pieces leaves run as work-queue
-  // kernels of <= 512 bodies, 16384 leaves (then 32768 when 16384 won and
-  // prepared in under 150 s); only when the whole count takes > 1 ms.
+  // kernels of <= 512 bodies: 32768 leaves (C5: 4096 / 16384 / 32768 /
+  // 65536 leaves -> 5.1 / 2.2 / 1.3 / 1.4 ms), 16384 if that lost and
+  // prepared quickly; only when the whole count takes > 1 ms.
   struct Trial { int sp, j, qb; float ms; double prep_s; };
   std::vector<Trial> kcof;
   if (best >= 0 && k_free >= 28) {
@@ -2244,8 +2252,8 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     for (int jj : {0, 4})
       if ((rc = trial(0, jj, 0))) break;
     if (!rc && bestt.ms > 1.0f) {
-      rc = trial(16384, 0, 512);
-      if (!rc && bestt.sp == 16384 && kcof.back().prep_s < 150.0) rc = trial(32768, 0, 512);
+      rc = trial(32768, 0, 512);
+      if (!rc && bestt.sp != 32768 && kcof.back().prep_s < 120.0) rc = trial(16384, 0, 512);
     }
     if (rc) p->opt = cands[best].o;
     p->opt.kernel_cofactor_bits = bestt.j;
