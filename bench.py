@@ -136,14 +136,14 @@ def oracle_rate(text, n, seconds, threads=None):
     a contiguous sub-cube of valuations sized for ~`seconds` of CPU work."""
     import oracle
     threads = threads or oracle.default_threads()
-    k = 14
+    k = min(14, n)
     while True:
         t0 = time.perf_counter()
         oracle.count(text, n, 0, 1 << k, threads=threads)
         dt = time.perf_counter() - t0
         if dt > 0.5 or k >= n:
             break
-        k += 2
+        k = min(k + 2, n)
     rate = (1 << k) / dt
     k2 = min(n, max(k, int(rate * seconds).bit_length() - 1))
     lo = (1 << n) - (1 << k2) if n > k2 else 0   # a sub-cube away from mu = 0
