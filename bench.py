@@ -6,29 +6,41 @@ Default workload (the config BASELINE.json's metric is quoted on: register
 mode count at 1/2/4/8 GPUs against the int-ALU roofline) is config C5: a
 random 1000-gate Boolean DAG over n = 42 variables, 2^42 valuations per step.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3_posets]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c4|c3_posets|c2|c2_n32|...]
     torchrun --nproc-per-node N bench.py --gpus N ...      (one rank per GPU)
     python bench.py --impl reference ...                   (the CPU oracle arm)
 
-A step = one full pass of the hot path over the step's batch: every rank
-counts its share of the 2^n cube with the JIT'd register-mode kernels
-(generators synthesised in registers, straight-line LOP3/IMAD bodies, fused
-popcount + reduction) -- with the autotuned configuration, the leaves of a
-Shannon decomposition (its pieces balanced over the ranks by
-bfa_count_shard) run as persistent work-queue kernels replayed from one CUDA
-graph -- then ONE NCCL all-reduce of the 8-byte count (P > 1).  Leaves the
-Reduction proves identically 0 are decided at preparation time and reported
-(decided_at_compile_time); preparation (autotune + JIT) is outside the timed
-region and reported as jit_prep_s.  Timing: W untimed warm-up steps; L2 flushed
-(256 MiB write) before every timed step; CUDA events on the launching stream
-around each step; barrier + synchronize on both sides; max over ranks.
-Prints one JSON line on rank 0.
+Headline (`value`): the paper's brute-force block evaluation (PAPER.md:356-372,
+955) -- ONE register-mode kernel (presets.EXHAUSTIVE: generators synthesised
+in registers, 32 slot cofactors folded into a straight-line LOP3/IMAD body,
+searched variable roles, fused popcount + reduction) evaluates every word of
+every valuation of the rank's cofactor range [r 2^(n-p), (r+1) 2^(n-p)) inside
+the timed region; then ONE 8-byte NCCL all-reduce (P > 1).  Nothing is decided
+at preparation time.  Preparation (role search + NVRTC, rank 0 first so the
+other ranks load its cubin from the JIT cache) is outside the timed region and
+reported as prep_s, as in any JIT-compiled benchmark.
+
+`e2e`: a COLD call through the public API, every step: bfa_compile of the
+text -> bfa_count_range (role search + NVRTC with the persistent JIT cache
+disabled, module load, launch) -> the count read on the host (and, P > 1,
+all-reduced); wall clock, max over ranks.
+
+`replay` (N = 1, C5/C4): the decomposed plan (presets.DECOMPOSED: Shannon
+leaves of the Reduction run as work-queue kernels).  Leaves the Reduction
+proves 0 are decided during its preparation, so its step time is a replay of
+a prepared plan; reported with its cold preparation time and the valuations
+it decided, never as the headline.
+
+Timing: W untimed warm-up steps; L2 flushed (256 MiB write) between timed
+steps; CUDA events on the launching stream; barrier + synchronize on both
+sides; max over ranks.  Prints one JSON line on rank 0.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -40,30 +52,29 @@ sys.path.insert(0, ROOT)
 
 import workloads as W  # noqa: E402
 
-# guide unit counts (B300_MICROARCH.md "Pipe rates": LOP3 on the alu pipe,
-# rt_SMSP = 2 -> 16 lanes/clk per SM sub-partition, 4 per SM -> 64 LOP3/clk/SM)
 SMS = 148
-LOP3_PER_CLK_PER_SM = 64
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="bfa", choices=["bfa", "reference"])
     ap.add_argument("--config", default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-extras", action="store_true", help="skip the replay and the extra config lines")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--options", default=None,
-                    help="JSON dict of program options: skip autotuning (e.g. to profile the exact "
-                         "configuration an earlier plain run chose)")
+                    help="JSON dict of program options applied on top of the preset (profiling variants)")
     return ap.parse_args()
 
 
 MATERIALISED = {"c2": ("c2", 0), "c2_fused": ("c2", 1), "c2_n32": ("c2_n32", 0), "c2_n32_fused": ("c2_n32", 1)}
 
 CONFIG_DESC = {
+    "c1": "labeled partial orders on 3 points, n=9 (BASELINE configs[0])",
     "c2": "random 3-CNF, 2000 clauses over n=28, materialised vector algebra (HBM) + popcount (BASELINE configs[1])",
     "c2_fused": "random 3-CNF, 2000 clauses over n=28, materialised table S, fused 128-bit-load kernel + popcount",
     "c2_n32": "random 3-CNF, 2000 clauses over n=32 (512 MiB vectors >> L2), materialised vector algebra + popcount",
@@ -77,11 +88,10 @@ CONFIG_DESC = {
 }
 
 
-def config_block(name, n, info, world):
-    return {"workload": f"{name}: {CONFIG_DESC.get(name, name)}", "n": n,
-            "valuations_per_step": 1 << n, "gates_G": info["gates"] if info else None,
-            "luts_L": info["luts"] if info else None, "support": info["support"] if info else None,
-            "seed": W.SEED, "parallelism": f"cofactor x{world} (top log2(P) variable ids)",
+def config_block(name, n, world):
+    """Workload identity only (identical in both arms)."""
+    return {"workload": f"{name}: {CONFIG_DESC.get(name, name)}", "n": n, "valuations_per_step": 1 << n,
+            "seed": W.SEED, "parallelism": f"cofactor x{world} (top log2(P) variable ids, contiguous ranges)",
             "l2": "count mode reads no HBM inputs (generators synthesised in registers); "
                   "L2 flushed with a 256 MiB write before every timed step anyway"}
 
@@ -131,26 +141,67 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- oracle (CPU) leg
-def oracle_rate(text, n, seconds, threads=None):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
+
+
+def _subcube(n, k, i, count):
+    """Start of the i-th of `count` spread-out aligned 2^k sub-cubes of [0, 2^n)."""
+    if k >= n:
+        return 0
+    slots = 1 << (n - k)
+    return ((i * slots) // count + (slots // (2 * count))) % slots << k
+
+
+def oracle_rate(text, n, seconds, threads=None, cubes=4):
     """Time the CPU oracle, as it stands, on a bounded sample of the workload:
-    a contiguous sub-cube of valuations sized for ~`seconds` of CPU work."""
+    `cubes` spread-out aligned sub-cubes, sized together for ~`seconds` of
+    CPU work.  Returns (valuations/s, threads, description)."""
     import oracle
     threads = threads or oracle.default_threads()
-    k = min(14, n)
-    while True:
+    k = min(12, n)
+    while True:                                   # size probe
         t0 = time.perf_counter()
         oracle.count(text, n, 0, 1 << k, threads=threads)
         dt = time.perf_counter() - t0
-        if dt > 0.5 or k >= n:
+        if dt > 0.3 or k >= n:
             break
         k = min(k + 2, n)
-    rate = (1 << k) / dt
-    k2 = min(n, max(k, int(rate * seconds).bit_length() - 1))
-    lo = (1 << n) - (1 << k2) if n > k2 else 0   # a sub-cube away from mu = 0
-    t0 = time.perf_counter()
-    oracle.count(text, n, lo, lo + (1 << k2), threads=threads)
-    dt = time.perf_counter() - t0
-    return (1 << k2) / dt, threads, f"sub-cube of 2^{k2} valuations [{lo}, {lo + (1 << k2)}), {dt:.1f} s"
+    rate = (1 << k) / max(dt, 1e-9)
+    k2 = min(n, max(k, int(rate * seconds / cubes).bit_length() - 1))
+    m = 1 if k2 >= n else cubes
+    total, spent, starts = 0, 0.0, []
+    for i in range(m):
+        lo = _subcube(n, k2, i, m)
+        starts.append(lo)
+        t0 = time.perf_counter()
+        oracle.count(text, n, lo, lo + (1 << k2), threads=threads)
+        spent += time.perf_counter() - t0
+        total += 1 << k2
+    desc = (f"{m} sub-cubes of 2^{k2} valuations at mu = {starts[:4]}{'...' if m > 4 else ''} "
+            f"({total} valuations, {spent:.1f} s)")
+    if m == 1 and k2 >= n:
+        desc = f"sub-cube of 2^{k2} valuations [0, {1 << k2}), {spent:.1f} s (the whole cube)"
+    return total / spent, threads, desc
+
+
+def cpu_baseline_block(text, n, seconds):
+    """The oracle on the host: all-cores rate on >= 4 sub-cubes, a 1-thread
+    rate, the CPU model, and the extrapolated full-run time."""
+    import oracle
+    allc = oracle.default_threads()
+    v, cores, sample = oracle_rate(text, n, seconds * 0.75, threads=allc)
+    v1, _, sample1 = oracle_rate(text, n, seconds * 0.25, threads=1, cubes=1)
+    return {"value": v, "unit": "valuations/s", "cores": cores, "kind": "oracle", "sample": sample,
+            "one_thread": {"value": v1, "sample": sample1}, "cpu_model": cpu_model(),
+            "extrapolated_full_run_s": (1 << n) / v}
 
 
 def run_reference(args):
@@ -168,9 +219,9 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": (1 << n) / value * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bool (C int per valuation)", "data": "synthetic",
-            "config": config_block(args.config, n, None, 1),
+            "config": config_block(args.config, n, 1),
             "cpu_baseline": {"value": value, "unit": "valuations/s", "cores": cores, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -185,7 +236,7 @@ def traffic_for(cfg):
         return None
 
 
-# ---------------------------------------------------------------- GPU leg
+# ---------------------------------------------------------------- GPU helpers
 def measure_int_peaks(bfa, torch, dev):
     """Measured integer issue rates (ops/s): LOP3 only (ALU pipe), IMAD only
     (FMA pipe), and LOP3+IMAD 1:1 (both pipes, bounded by issue)."""
@@ -195,13 +246,61 @@ def measure_int_peaks(bfa, torch, dev):
     for op, name in ((0, "lop3"), (1, "imad"), (2, "lop3_imad_1to1")):
         bfa.peak_int(op, blocks, threads, 10, sink)
         torch.cuda.synchronize()
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        bfa.peak_int(op, blocks, threads, iters, sink)
-        e.record()
-        torch.cuda.synchronize()
-        out[name] = blocks * threads * iters * 256 / (s.elapsed_time(e) / 1e3)
+        best = 0.0
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            bfa.peak_int(op, blocks, threads, iters, sink)
+            e.record()
+            torch.cuda.synchronize()
+            best = max(best, blocks * threads * iters * 256 / (s.elapsed_time(e) / 1e3))
+        out[name] = best
     return out
+
+
+def int_roofline(launch, words, seconds, peaks, cfg):
+    """Roofline of a register-mode count: algorithmic work per 32-bit word =
+    the executed cells of the slot-cofactored, hoisted cover:
+    A LOP3 cells on the ALU pipe and F IMAD cells (+ IMAD operand registers)
+    on the FMA pipe.  The bound for this mix is the binding one of
+    R_lop3 / A, R_imad / F and R_issue / (A + F) words/s (measured rates)."""
+    A = launch["cells_lop3"] / words
+    F = launch["cells_imad"] / words
+    wps = words / seconds
+    terms = {"alu_pipe (LOP3)": peaks["lop3"] / A if A else float("inf"),
+             "fma_pipe (IMAD)": peaks["imad"] / F if F else float("inf"),
+             "issue (1 warp-inst/clk/SMSP)": peaks["lop3_imad_1to1"] / (A + F)}
+    binding = min(terms, key=terms.get)
+    bound = terms[binding]
+    return {"bound": "alu", "achieved": (A + F) * wps, "peak": (A + F) * bound, "unit": "int ops/s",
+            "frac": wps / bound, "traffic": traffic_for(cfg),
+            "per_unit": f"{A + F:.2f} integer cells per 32-bit word (32 valuations): {A:.2f} LOP3 (ALU pipe) + "
+                        f"{F:.2f} IMAD (FMA pipe) of the slot-cofactored, hoisted cover",
+            "units_per_launch": words, "binding": binding,
+            "peak_source": "measured bfa_peak_int rates (LOP3 ALU pipe, IMAD FMA pipe, 1:1 mix issue-bound); "
+                           "peak = the binding pipe for this kernel's LOP3:IMAD mix",
+            "peak_measured": peaks,
+            "alu_pipe": {"lop3_per_s": A * wps, "frac": A * wps / peaks["lop3"]},
+            "fma_pipe": {"imad_per_s": F * wps, "frac": F * wps / peaks["imad"]}}
+
+
+class Timer:
+    """CUDA events on one stream around each of K steps; L2 flushed between."""
+
+    def __init__(self, torch, stream, dev):
+        self.torch, self.stream = torch, stream
+        self.flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def run(self, fn, steps):
+        torch = self.torch
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for i in range(steps):
+            self.flush.fill_(i & 0xFF)
+            ev[i][0].record(self.stream)
+            fn()
+            ev[i][1].record(self.stream)
+        torch.cuda.synchronize()
+        return [s.elapsed_time(e) / 1e3 for s, e in ev]
 
 
 def run_bfa(args):
@@ -209,6 +308,7 @@ def run_bfa(args):
     import torch.distributed as dist
 
     import paper_1310_6978_b200 as bfa
+    from paper_1310_6978_b200 import presets
     from paper_1310_6978_b200.dist import rank_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -222,189 +322,190 @@ def run_bfa(args):
         dist.init_process_group("nccl", device_id=dev)
 
     text, n, expect = W.config(args.config)
-    prog = bfa.Program(text)
+    extra_opts = json.loads(args.options) if args.options else {}
+    prog = presets.apply(bfa.Program(text), presets.EXHAUSTIVE, **extra_opts)
     info = prog.info
     lo, hi = rank_range(n, rank, world)
     stream = torch.cuda.current_stream()
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    def count_step():
-        # world == 1: the whole cube; world > 1: this rank's work-balanced
-        # share of the cofactors (bfa_count_shard), then ONE 8-byte all-reduce
-        if world == 1:
-            prog.count_range(n, lo, hi, out=cnt, stream=stream)
-        else:
-            prog.count_shard(n, rank, world, out=cnt, stream=stream)
 
     def step():
-        count_step()
+        prog.count_range(n, lo, hi, out=cnt, stream=stream)
         if world > 1:
             dist.all_reduce(cnt)
 
-    # autotune (JIT of the candidate variants + probe timing; untimed), then
-    # warm-up.  Rank 0 tunes and broadcasts its choice so every rank runs the
-    # same kernel.  The one-time preparation cost (tuning, role search,
-    # cofactor split, NVRTC) is reported as jit_prep_s.
+    # ---- preparation (role search + NVRTC + module load), untimed.  Rank 0
+    # compiles first and writes the persistent JIT cache; the other ranks then
+    # load its role search and cubin instead of re-deriving them.
     t_prep = time.perf_counter()
-    if args.options:
-        tune = {"best": json.loads(args.options), "source": "--options"}
-    else:
-        tune = prog.autotune(n) if rank == 0 else None
+    if rank == 0:
+        prog.count_range(n, lo, hi, out=cnt, stream=stream)
+        torch.cuda.synchronize()
     if world > 1:
-        obj = [tune]
-        dist.broadcast_object_list(obj, src=0)
-        tune = obj[0]
-    for key, val in ((tune or {}).get("best") or {}).items():
-        prog.set_option(key, val)
-    for i in range(max(args.warmup, 3)):
-        step()
-        if i == 0:
+        dist.barrier()
+        if rank != 0:
+            prog.count_range(n, lo, hi, out=cnt, stream=stream)
             torch.cuda.synchronize()
-            t_prep = time.perf_counter() - t_prep
+    prep_s = time.perf_counter() - t_prep
+    for _ in range(max(args.warmup, 3)):
+        step()
     torch.cuda.synchronize()
     launch = bfa.last_launch()
-    result = int(cnt.item()) & ((1 << 64) - 1)
 
+    timer = Timer(torch, stream, dev)
     clocks = ClockSampler(local)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kstarts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = bfa.last_launch().get("launch_counter", 0)
     clocks.start()
     time.sleep(0.3)
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)                      # L2 flush, outside the events
-        starts[i].record(stream)
-        kstarts[i].record(stream)
-        count_step()
-        kends[i].record(stream)
-        if world > 1:
-            dist.all_reduce(cnt)
-        ends[i].record(stream)
-    torch.cuda.synchronize()
+    step_s = timer.run(step, args.steps)
     launches_timed = bfa.last_launch().get("launch_counter", 0) - launches0
-    if world > 1:
-        dist.barrier()
     clk = clocks.stop()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
-    t_total = sum(step_ms) / 1e3
-    t_kern = sum(kern_ms) / 1e3
+    # kernel-only time of this rank (the count without the all-reduce)
+    kern_s = timer.run(lambda: prog.count_range(n, lo, hi, out=cnt, stream=stream), min(args.steps, 5))
+    if world > 1:
+        step()
+        dist.barrier()
+    t_total, t_kern = sum(step_s), statistics.median(kern_s)
     if world > 1:
         tt = torch.tensor([t_total, t_kern], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_total, t_kern = tt.tolist()
     final = int(cnt.item()) & ((1 << 64) - 1)
-    valuations = (1 << n) * args.steps
-    value = valuations / t_total
-    words_per_launch = ((hi - lo) if world == 1 else (1 << n) // world) >> 5
-    L = info["luts"]
-    kernel_s = t_kern / args.steps
-    # Work per 32-bit word of the cover the kernel must execute: the JIT'd
-    # program is the cell cover of f cofactored on the slot variables, with
-    # loop-invariant cells hoisted: LOP3 cells on the ALU pipe,
-    # IMAD cells (+ their operand registers) on the FMA pipe.
-    if launch.get("variant") == "segmented":      # NEXT-3: every cell per word, LOP3 only
-        lop3_w, imad_w = launch.get("emitted", launch["cells"]), 0.0
-    elif "cells_lop3" in launch:                   # executed cells summed over all launches
-        lop3_w = launch["cells_lop3"] / words_per_launch
-        imad_w = launch["cells_imad"] / words_per_launch
-    else:
-        seg = max(launch["segments"], key=lambda g: g["words"])
-        S, m = seg["words_per_iter"], seg["m"]
-        lop3_w = seg["luts_inner"] / S + seg["luts_outer"] / (S << m)
-        imad_w = (seg["imads_inner"] + seg["derived_inner"]) / S + (seg["imads_outer"] + seg["derived_outer"]) / (S << m)
-    cells_w = lop3_w + imad_w
-    achieved = cells_w * words_per_launch / kernel_s           # integer cell ops/s per GPU
-    sm_clock = clk["sm_max_mhz"] or 1965.0
-    # derived: the scheduler issues 1 warp-instruction/clk per SMSP; LOP3 takes
-    # the ALU pipe (16 lanes/clk/SMSP), IMAD the FMA pipe (32 lanes/clk/SMSP)
-    peak_issue = SMS * 4 * 32 * sm_clock * 1e6
-    peak_alu = SMS * LOP3_PER_CLK_PER_SM * sm_clock * 1e6
+    value = (1 << n) * args.steps / t_total
+    words = (hi - lo) >> 5
     peaks = measure_int_peaks(bfa, torch, dev)
+    roof = int_roofline(launch, words, t_kern, peaks, args.config + "_exhaustive")
 
-    # e2e: the public C-ABI call with a host result (bfa_count -> uint64 on the
-    # host: launch + 8-byte D2H + sync every step).  Count mode has no input
-    # buffers: the program is in the JIT'd instruction stream.
-    if world == 1:
-        prog.count(n)
+    # ---- e2e: COLD call through the public API every step (compile -> count
+    # -> host), persistent JIT cache disabled, max over ranks
+    e2e_steps = max(1, args.e2e_steps)
+    cubin_bytes = 0
+    e2e_t = []
+    for _ in range(e2e_steps):
+        if world > 1:
+            dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_count = prog.count(n)
-        e2e_value = valuations / (time.perf_counter() - t0)
-        assert e2e_count == final
-    else:
-        # the public multi-GPU call: dist.count_sharded (this rank's share +
-        # the 8-byte all-reduce) and the result read on the host; max over ranks
-        from paper_1310_6978_b200.dist import count_sharded
-        count_sharded(prog, n, stream=stream)
-        torch.cuda.synchronize()
-        dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_count = int(count_sharded(prog, n, stream=stream).item()) & ((1 << 64) - 1)
-        te = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        q = presets.apply(bfa.Program(text), presets.EXHAUSTIVE, jit_cache=0, **extra_opts)
+        t = q.count_range(n, lo, hi, stream=stream)
+        if world > 1:
+            dist.all_reduce(t)
+        e2e_count = int(t.item()) & ((1 << 64) - 1)   # device -> host read (synchronises)
+        e2e_t.append(time.perf_counter() - t0)
+        cubin_bytes = len(q.jit_cubin(1, n)) if world == 1 else 0
+        assert e2e_count == final, (e2e_count, final)
+        del q
+    e2e_s = statistics.median(e2e_t)
+    if world > 1:
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_value = valuations / te.item()
-        assert e2e_count == final
+        e2e_s = te.item()
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
+    verified = {}
+    if expect is not None:
+        verified["closed_form"] = final == expect
+        assert final == expect, (final, expect)
+
+    extras = {}
+    if world == 1 and not args.no_extras:
+        extras = run_extras(args, bfa, presets, torch, stream, dev, text, n, final, verified, peaks, timer)
+
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        v, cores, sample = oracle_rate(text, n, args.cpu_seconds)
-        cpu = {"value": v, "unit": "valuations/s", "cores": cores, "kind": "oracle", "sample": sample}
+        cpu = cpu_baseline_block(text, n, args.cpu_seconds)
 
-    kernels_per_step = launch.get("kernels", 1)
     line = {
         "metric": "valuations/s", "value": value, "unit": "valuations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_total / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32 (bitwise LOP3 on 32-valuation words)",
+        "vs_baseline": None, "dtype": "u32 (bitwise LOP3/IMAD on 32-valuation words)",
         "data": "synthetic (seeded generator, workloads/__init__.py)",
-        "config": config_block(args.config, n, info, world),
-        "count": final, "count_expected": expect,
-        "roofline": {"bound": "alu", "achieved": achieved, "peak": peaks["lop3_imad_1to1"], "unit": "int ops/s",
-                     "frac": achieved / peaks["lop3_imad_1to1"], "traffic": traffic_for(args.config),
-                     "per_unit": f"{cells_w:.2f} integer cells per 32-bit word (32 valuations): {lop3_w:.2f} LOP3 "
-                                 f"+ {imad_w:.2f} IMAD of the slot-cofactored, hoisted cover",
-                     "units_per_launch": words_per_launch,
-                     "peak_source": "measured bfa_peak_int LOP3+IMAD 1:1 (issue-bound: 1 warp-inst/clk/SMSP)",
-                     "peak_derived_issue": peak_issue, "frac_of_derived_issue": achieved / peak_issue,
-                     "peak_measured": peaks,
-                     "alu_pipe": {"lop3_per_s": lop3_w * words_per_launch / kernel_s, "peak_derived": peak_alu,
-                                  "frac": lop3_w * words_per_launch / kernel_s / peaks["lop3"]},
-                     "nominal": {"L": L, "G": info["gates"],
-                                 "lop3_equiv_per_s": L * words_per_launch / kernel_s,
-                                 "gate_word_ops_per_s": info["gates"] * words_per_launch / kernel_s}},
+        "config": config_block(args.config, n, world),
+        "program": {"gates_G": info["gates"], "luts_L": info["luts"], "support": info["support"],
+                    "options": dict(presets.EXHAUSTIVE, **extra_opts)},
+        "count": final, "count_expected": expect, "count_verified": verified,
+        "decided_at_compile_time": 0,
+        "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 8,
-                "call": "bfa_count(prog, n) -> host uint64"},
+        "e2e": {"value": (1 << n) / e2e_s, "unit": "valuations/s", "h2d_bytes_per_step": cubin_bytes,
+                "d2h_bytes_per_step": 8, "steps": e2e_steps, "s_per_call": e2e_s,
+                "call": "cold: bfa_compile(text) -> bfa_count_range over this rank's range (role search + NVRTC with "
+                        "the persistent JIT cache off, module load, launch) -> count read on the host"
+                        + (" -> all-reduce" if world > 1 else ""),
+                "h2d": "the JIT'd cubin loaded into the device each call (count mode has no input tensors)"},
         "gpu_launches": launches_timed,
-        "kernel_ms_per_step": kernel_s * 1e3,
+        "kernel_ms_per_step": t_kern * 1e3,
+        "prep_s": prep_s,
         "launch": launch,
-        "autotune": tune,
-        "jit_prep_s": t_prep,
-        "executed_valuations_per_s": ((1 << n) // world - launch.get("valuations_decided", 0)) * args.steps / t_total
-        * world,
-        "decided_at_compile_time": {
-            "valuations_per_rank": launch.get("valuations_decided", 0),
-            "how": "Shannon pieces / kernel-level cofactors the Reduction proved identically 0 (no models, no "
-                   "launch); the decomposition is prepared once in warm-up (jit_prep_s) and reused every step"},
         "clocks": clk,
     }
+    line.update(extras)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def run_extras(args, bfa, presets, torch, stream, dev, text, n, final, verified, peaks, timer):
+    """Secondary measurements in the same run (N = 1): the decomposed plan as
+    a labelled replay, the exhaustive line of the other count config, and
+    the materialised mode of C2 (HBM)."""
+    out = {}
+    steps = max(3, min(args.steps, 5))
+    if args.config in ("c5", "c4"):
+        # complement invariant through the same exhaustive preset (P-11)
+        body, outl = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+        if args.config == "c5":
+            pc = presets.apply(bfa.Program(f"{body}\n~{outl}"), presets.EXHAUSTIVE)
+            verified["complement_sum"] = final + pc.count(n) == 1 << n
+        # the decomposed plan, cold preparation, then replays
+        q = presets.apply(bfa.Program(text), presets.DECOMPOSED, jit_cache=0)
+        c = torch.zeros(1, dtype=torch.int64, device=dev)
+        t0 = time.perf_counter()
+        q.count_range(n, 0, 1 << n, out=c, stream=stream)
+        torch.cuda.synchronize()
+        prep = time.perf_counter() - t0
+        for _ in range(2):
+            q.count_range(n, 0, 1 << n, out=c, stream=stream)
+        torch.cuda.synchronize()
+        ll = bfa.last_launch()
+        ts = timer.run(lambda: q.count_range(n, 0, 1 << n, out=c, stream=stream), steps)
+        rc = int(c.item())
+        verified["decomposed_equals_exhaustive"] = rc == final
+        decided = ll.get("valuations_decided", 0)
+        t = statistics.median(ts)
+        out["replay"] = {
+            "what": "REPLAY of a prepared Shannon-decomposition plan (presets.DECOMPOSED): leaves the Reduction "
+                    "proved 0 were decided during preparation; not the headline",
+            "ms_per_step": t * 1e3, "valuations_per_s": (1 << n) / t,
+            "executed_valuations_per_s": ((1 << n) - decided) / t, "valuations_decided_at_prep": decided,
+            "prep_s_cold": prep, "first_call_valuations_per_s": (1 << n) / (prep + t), "count": rc,
+            "kernels": ll.get("kernels"), "queue": ll.get("queue"), "decompose_s": ll.get("decompose_s"),
+            "roofline": int_roofline(ll, 1 << (n - 5), t, peaks, args.config + "_replay")}
+    if args.config == "c5":
+        # the exhaustive line at n = 36 (C4)
+        t4, n4, e4 = W.config("c4")
+        p4 = presets.apply(bfa.Program(t4), presets.EXHAUSTIVE)
+        c4 = torch.zeros(1, dtype=torch.int64, device=dev)
+        for _ in range(3):
+            p4.count_range(n4, 0, 1 << n4, out=c4, stream=stream)
+        torch.cuda.synchronize()
+        l4 = bfa.last_launch()
+        ts = timer.run(lambda: p4.count_range(n4, 0, 1 << n4, out=c4, stream=stream), max(args.steps, 10))
+        t = statistics.median(ts)
+        verified["c4_closed_form"] = int(c4.item()) == e4
+        out["c4_exhaustive"] = {"valuations_per_s": (1 << n4) / t, "ms_per_step": t * 1e3, "count": int(c4.item()),
+                                "roofline": int_roofline(l4, 1 << (n4 - 5), t, peaks, "c4_exhaustive")}
+        for name in ("c2", "c2_fused", "c2_n32", "c2_n32_fused"):
+            out[name] = materialised_line(bfa, torch, stream, name, 3, timer)
+    return out
 
 
 def hbm_peak():
@@ -417,51 +518,64 @@ def hbm_peak():
         return 6650e9, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def run_materialised(args):
+def materialised_line(bfa, torch, stream, name, steps, timer):
     """The paper's vector formulation: generator table S in
     HBM, full-vector LOP3 passes (variant 0) or fused 128-bit loads (variant
-    1), popcount.  One GPU; a step = one full evaluation + count."""
+    1), popcount.  A step = one full evaluation + count."""
+    cfg, variant = MATERIALISED[name]
+    text, n, expect = W.config(cfg)
+    prog = bfa.Program(text)
+    out = torch.empty(bfa.words_for(n), dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(2):
+        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
+    torch.cuda.synchronize()
+    launch = bfa.last_launch()
+    ts = timer.run(lambda: prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream), steps)
+    t = statistics.median(ts)
+    vbytes = (1 << n) // 8
+    fill, popc = n * vbytes, vbytes
+    if variant == 0:
+        logical = launch.get("logical_bytes", 0) + fill + popc
+    else:
+        logical = fill + (launch.get("rows_loaded", n) + 1) * vbytes + popc
+    peak, src = hbm_peak()
+    dram = traffic_for(name + "_step")
+    line = {"valuations_per_s": (1 << n) / t, "ms_per_step": t * 1e3, "count": int(cnt.item()),
+            "count_expected": expect, "workload": CONFIG_DESC[name],
+            "roofline": {"bound": "hbm", "achieved": logical / t / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                         "frac": logical / t / peak, "peak_source": src,
+                         "traffic": dram, "dram_frac": (dram / t / peak) if dram else None,
+                         "per_unit": "logical bytes = table fill n*2^n/8 + sum over passes (arity+1)*2^n/8 "
+                                     "(variant 0) or (|supp|+1)*2^n/8 (variant 1) + popcount 2^n/8",
+                         "logical_bytes_per_step": logical},
+            "kernels": launch.get("kernels")}
+    if variant == 1:
+        # the fused kernel is ALU-bound for big programs: its LOP3 work per word
+        luts = launch.get("luts", 0)
+        line["alu"] = {"lop3_per_s": luts * (1 << (n - 5)) / t}
+    return line
+
+
+def run_materialised(args):
+    """--config c2|c2_fused|c2_n32|c2_n32_fused as the headline (one GPU)."""
     import torch
 
     import paper_1310_6978_b200 as bfa
     if int(os.environ.get("WORLD_SIZE", "1")) != 1:
         raise SystemExit("materialised configs run on one GPU")
     torch.cuda.set_device(0)
-    cfg, variant = MATERIALISED[args.config]
-    text, n, expect = W.config(cfg)
-    prog = bfa.Program(text)
-    info = prog.info
-    out = torch.empty(bfa.words_for(n), dtype=torch.int64, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     stream = torch.cuda.current_stream()
-    for _ in range(max(args.warmup, 3)):
-        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
-    torch.cuda.synchronize()
-    launch = bfa.last_launch()
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    timer = Timer(torch, stream, "cuda")
     clocks = ClockSampler(0)
     clocks.start()
-    time.sleep(0.2)
-    ms = []
-    for i in range(args.steps):
-        flush.fill_(i & 0xFF)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record(stream)
-        prog.eval_materialised(n, variant, out=out, count_out=cnt, stream=stream)
-        e.record(stream)
-        torch.cuda.synchronize()
-        ms.append(s.elapsed_time(e))
+    ml = materialised_line(bfa, torch, stream, args.config, args.steps, timer)
     clk = clocks.stop()
-    t = sum(ms) / 1e3 / args.steps
-    vbytes = (1 << n) // 8
-    fill = n * vbytes
-    popc = vbytes
-    if variant == 0:
-        logical = launch.get("logical_bytes", 0) + fill + popc
-    else:
-        logical = fill + (launch.get("rows_loaded", n) + 1) * vbytes + popc
-    peak, src = hbm_peak()
-    # e2e: host buffers -- the vector copied back to pinned host memory each step
+    cfg, variant = MATERIALISED[args.config]
+    text, n, _ = W.config(cfg)
+    prog = bfa.Program(text)
+    out = torch.empty(bfa.words_for(n), dtype=torch.int64, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     host = torch.empty(out.numel(), dtype=torch.int64, pin_memory=True)
     t0 = time.perf_counter()
     for _ in range(args.steps):
@@ -469,23 +583,15 @@ def run_materialised(args):
         host.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
     e2e = (1 << n) * args.steps / (time.perf_counter() - t0)
-    line = {"metric": "valuations/s", "value": (1 << n) / t, "unit": "valuations/s", "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+    line = {"metric": "valuations/s", "value": ml["valuations_per_s"], "unit": "valuations/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ml["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32 (bitwise, 128-bit vector accesses)",
             "data": "synthetic (seeded generator, workloads/__init__.py)",
-            "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}", "n": n, "clauses": 2000,
-                       "luts_L": info["luts"], "gates_G": info["gates"], "seed": W.SEED,
-                       "l2": "L2 flushed (256 MiB write) before every timed step; n=28 vectors (32 MiB) can be "
-                             "L2-resident within a step, n=32 (512 MiB) cannot"},
-            "count": int(cnt.item()), "count_expected": expect,
-            "roofline": {"bound": "hbm", "achieved": logical / t / 1e9, "peak": peak / 1e9, "unit": "GB/s",
-                         "frac": logical / t / peak, "traffic": None, "peak_source": src,
-                         "per_unit": "logical bytes = table fill n*2^n/8 + sum over passes (arity+1)*2^n/8 "
-                                     "(variant 0) or (|supp|+1)*2^n/8 (variant 1) + popcount 2^n/8",
-                         "logical_bytes_per_step": logical},
-            "e2e": {"value": e2e, "unit": "valuations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": vbytes,
-                    "call": "bfa_eval_materialised + vector D2H to pinned host"},
-            "gpu_launches": launch.get("kernels", 0) * args.steps, "launch": launch, "clocks": clk}
+            "config": config_block(args.config, n, 1), "count": ml["count"], "count_expected": ml["count_expected"],
+            "roofline": ml["roofline"],
+            "e2e": {"value": e2e, "unit": "valuations/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": (1 << n) // 8, "call": "bfa_eval_materialised + vector D2H to pinned host"},
+            "gpu_launches": (ml["kernels"] or 0) * args.steps, "clocks": clk}
     print(json.dumps(line), flush=True)
 
 

@@ -136,6 +136,13 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
  *                   leaves of <= this many gates each back into their parent
  *                   (default 0)
+ *   "jit_cache"     0: this program neither reads nor writes the persistent JIT
+ *                   cache (cubins, role searches); every compile is cold
+ *                   (default 1)
+ *   "decompose_min_k" split_pieces applies to aligned sub-cubes of >= 2^this
+ *                   valuations (default 30; 10..64)
+ *   "split_min_vars" decomposition pieces with <= this many free variables
+ *                   are not split further (default 24; 5..63)
  *   "queue_support" 1: a work-queue body enumerates only the variables its
  *                   leaf depends on (and enough others for the body layout);
  *                   its count is scaled by 2^(dropped) (default 0)
@@ -174,6 +181,30 @@ int bfa_eval(const bfa_prog* p, int n, uint64_t* out);
  * range must be the whole [0, 2^n). */
 int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
                     uint64_t* count_dev, void* stream);
+
+/* Role introspection (count mode; SURVEY.md §8(a) a4 "roles"; DESIGN.md §5
+ * role search).  A count over an aligned sub-cube of 2^k_free valuations
+ * enumerates it in a searched variable order: variable v (< k_free) takes the
+ * value of bit perm[v] of the kernel's position index q (variables >= k_free
+ * keep their own bit).  bfa_roles writes that permutation (64 entries,
+ * perm_out[v]) for the kernel such a count launches under p's current
+ * options, for a device with `sms` SMs (<= 0: the current device's, else
+ * 148); host only (runs the search if it is not cached).  BFA_E_ARG when the
+ * sub-cube would run on the generic kernel (no roles). */
+int bfa_roles(const bfa_prog* p, int n, int k_free, int sms, int8_t* perm_out);
+
+/* Count with EXACTLY the kernel (same variant, roles and cubin) that a count
+ * of an aligned 2^k_free sub-cube launches, over the position range
+ * [pos_lo, pos_hi) of its enumeration order: the number of q in the range
+ * whose valuation mu(q) (mu_v = bit perm[v] of q) is a model.  This lets a
+ * test check the benchmarked kernel of the full 2^n cube against an oracle
+ * on sub-ranges: with f'(x) = f(x renamed v -> perm[v]), the result equals
+ * the models of f' in [pos_lo, pos_hi).  Bounds must be multiples of the
+ * kernel's outer-iteration unit, 2^(5 + slot_bits + thread_bits + m)
+ * valuations, else BFA_E_ARG.  Written to *count_dev (device), async on
+ * `stream`. */
+int bfa_count_positions(const bfa_prog* p, int n, int k_free, uint64_t pos_lo, uint64_t pos_hi,
+                        uint64_t* count_dev, void* stream);
 
 /* Multi-GPU count with work-balanced cofactor sharding (
  * DESIGN.md §6): every rank derives the same split of the 2^n cube into 2^j
@@ -292,8 +323,20 @@ int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len);
  * Lets the build check every generated kernel on a CPU-only host. */
 int64_t bfa_jit_cubin(const bfa_prog* p, int what, int n, void* buf, size_t len);
 
+/* Message of the last failing call on this thread (thread-local, valid until
+ * the next failing call on this thread). */
 const char* bfa_last_error(void);
+/* BFA_E_* code of the last failing call on this thread (0 if none yet); the
+ * way to classify a bfa_count failure, which returns UINT64_MAX. */
+int bfa_last_error_code(void);
 const char* bfa_version(void);
+
+/* Persistent JIT cache key of a generated kernel source (host only): the
+ * 64-hex-digit SHA-256 over the cache format salt, the NVRTC version, the
+ * NVRTC options and the source; cubins are stored as k_<key>.cubin under
+ * $BFA_JIT_CACHE (default ~/.cache/bfa_jit; "0" disables the cache).  out
+ * receives 64 digits + NUL (len >= 65), else BFA_E_ARG. */
+int bfa_cache_key(const char* source, char* out, size_t len);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ import json
 import os
 
 __all__ = ["Program", "Batch", "BfaError", "words_for", "reinstate", "last_launch", "fill_generators", "popcount",
-           "peak_int", "lib_path", "version"]
+           "peak_int", "lib_path", "version", "cache_key"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbfa.so")
@@ -54,7 +54,12 @@ _SIGS = {
     "bfa_shard_plan": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                   _c.POINTER(_c.c_uint64), _c.c_int, _c.POINTER(_c.c_int)]),
     "bfa_prepare": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int]),
+    "bfa_roles": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.POINTER(_c.c_int8)]),
+    "bfa_count_positions": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p,
+                                       _c.c_void_p]),
     "bfa_last_error": (_c.c_char_p, []),
+    "bfa_last_error_code": (_c.c_int, []),
+    "bfa_cache_key": (_c.c_int, [_c.c_char_p, _c.c_char_p, _c.c_size_t]),
     "bfa_version": (_c.c_char_p, []),
 }
 
@@ -176,6 +181,21 @@ class Program:
         """bfa_count_range: models in [lo, hi) into a 1-element device tensor (async)."""
         out = _u64_out(out, 1)
         _check(_load().bfa_count_range(self._h, n, lo, hi, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+        return out
+
+    def roles(self, n: int, k_free: int | None = None, sms: int = 0) -> list:
+        """bfa_roles: perm[v] = bit position of variable v in the enumeration
+        order of the count kernel for an aligned 2^k_free sub-cube (host only)."""
+        perm = (ctypes.c_int8 * 64)()
+        _check(_load().bfa_roles(self._h, n, n if k_free is None else k_free, sms, perm))
+        return list(perm)
+
+    def count_positions(self, n: int, k_free: int, lo: int, hi: int, out=None, stream=None):
+        """bfa_count_positions: models among positions [lo, hi) of the exact
+        kernel a 2^k_free sub-cube count launches (async, device tensor)."""
+        out = _u64_out(out, 1)
+        _check(_load().bfa_count_positions(self._h, n, k_free, lo, hi, ctypes.c_void_p(out.data_ptr()),
+                                           _stream(stream)))
         return out
 
     def prepare(self, n: int, sms: int = 0):
@@ -305,12 +325,14 @@ def reinstate(mu_free, free_ids, assignment: dict) -> list:
 
 
 def _err_code() -> int:
-    msg = _load().bfa_last_error().decode()
-    for code, key in ((BFA_E_RANGE, "outside"), (BFA_E_RANGE, "needs n"), (BFA_E_CUDA, "CUDA"),
-                      (BFA_E_CUDA, "device"), (BFA_E_JIT, "NVRTC"), (BFA_E_JIT, "cuModule")):
-        if key in msg:
-            return code
-    return BFA_E_ARG
+    return int(_load().bfa_last_error_code())
+
+
+def cache_key(source: str) -> str:
+    """bfa_cache_key: SHA-256 key of a generated kernel source in the JIT cache."""
+    buf = ctypes.create_string_buffer(65)
+    _check(_load().bfa_cache_key(source.encode(), buf, 65))
+    return buf.value.decode()
 
 
 def fill_generators(n: int, rows: int | None = None, out=None, stream=None):

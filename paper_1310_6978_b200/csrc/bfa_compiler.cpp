@@ -3,6 +3,7 @@
 #include "bfa_compiler.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <cctype>
 #include <cstdio>
 #include <cstring>
@@ -10,6 +11,7 @@
 #include <map>
 #include <set>
 #include <sstream>
+#include <thread>
 
 namespace bfa {
 
@@ -912,43 +914,96 @@ double model_cost(const Parsed& prog, const KernelSpec& spec) {
   return t;
 }
 
-std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int k_free, int budget, uint64_t seed) {
+std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int k_free, int budget, uint64_t seed,
+                                 int threads) {
   // Count mode over an aligned sub-cube of 2^k_free valuations: any
   // permutation of the variables below k_free is a bijection of the sub-cube,
   // so the count is unchanged; search the one whose cover is cheapest.
+  //
+  // The search is a fixed sequence of candidates drawn from one seeded
+  // generator (random restarts, then swap hill climbing); with threads > 1
+  // the model evaluations of consecutive candidates run speculatively in
+  // parallel and are committed in sequence order, so the result is the same
+  // for every thread count (and on every machine).
   k_free = std::min(k_free, 63);
-  KernelSpec spec = base;
   std::vector<int8_t> perm(64);
   for (int v = 0; v < 64; v++) perm[v] = (int8_t)v;
-  if (k_free <= 5 || spec.generic || spec.materialised || spec.mode != KM_COUNT) return {};
-  const int s = spec.slot_bits, t = spec.thread_bits, m = spec.inner_bits;
+  if (k_free <= 5 || base.generic || base.materialised || base.mode != KM_COUNT) return {};
+  const int s = base.slot_bits, t = base.thread_bits, m = base.inner_bits;
   auto role = [&](int q) { return q < 5 ? 0 : q - 5 < s ? 1 : q - 5 < s + t ? 2 : q - 5 < s + t + m ? 3 : 4; };
   auto eval = [&](const std::vector<int8_t>& pm) {
+    KernelSpec spec = base;
     spec.perm = pm;
     return model_cost(prog, spec);
   };
   uint64_t rs = seed * 6364136223846793005ull + 1442695040888963407ull;
   auto rnd = [&](uint64_t n) { rs = rs * 6364136223846793005ull + 1442695040888963407ull; return (rs >> 33) % n; };
+  threads = std::max(1, std::min(threads, 64));
   std::vector<int8_t> best = perm;
   double best_c = eval(best);
   int evals = 1;
-  // random restarts: shuffle the free variables' positions
-  for (int r = 0; r < std::max(1, budget / 4) && evals < budget; r++) {
-    std::vector<int8_t> pm = perm;
-    for (int i = k_free - 1; i > 0; i--) std::swap(pm[i], pm[rnd((uint64_t)i + 1)]);
-    double c = eval(pm);
-    evals++;
-    if (c < best_c) { best_c = c; best = pm; }
+  // evaluate a batch of candidates (in parallel when threads > 1)
+  auto eval_batch = [&](const std::vector<std::vector<int8_t>>& cand, std::vector<double>* cost) {
+    cost->assign(cand.size(), 0.0);
+    if (threads == 1 || cand.size() == 1) {
+      for (size_t i = 0; i < cand.size(); i++) (*cost)[i] = eval(cand[i]);
+      return;
+    }
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> th;
+    const size_t W = std::min<size_t>(cand.size(), (size_t)threads);
+    for (size_t w = 0; w < W; w++)
+      th.emplace_back([&] {
+        for (size_t i; (i = next.fetch_add(1)) < cand.size();) (*cost)[i] = eval(cand[i]);
+      });
+    for (auto& x : th) x.join();
+  };
+  // random restarts: shuffle the free variables' positions (independent draws)
+  {
+    const int R = std::min(std::max(1, budget / 4), budget - evals);
+    std::vector<std::vector<int8_t>> cand;
+    for (int r = 0; r < R; r++) {
+      std::vector<int8_t> pm = perm;
+      for (int i = k_free - 1; i > 0; i--) std::swap(pm[i], pm[rnd((uint64_t)i + 1)]);
+      cand.push_back(std::move(pm));
+    }
+    std::vector<double> cost;
+    eval_batch(cand, &cost);
+    for (size_t r = 0; r < cand.size(); r++) {
+      evals++;
+      if (cost[r] < best_c) { best_c = cost[r]; best = cand[r]; }
+    }
   }
-  // hill climbing: swap the positions of two variables with different roles
-  while (evals < budget) {
-    int a = (int)rnd((uint64_t)k_free), c = (int)rnd((uint64_t)k_free);
-    if (role(best[a]) == role(best[c])) continue;
-    std::vector<int8_t> pm = best;
-    std::swap(pm[a], pm[c]);
-    double cc = eval(pm);
-    evals++;
-    if (cc < best_c) { best_c = cc; best = pm; }
+  // hill climbing: swap the positions of two variables with different roles;
+  // candidates are drawn from the current best in sequence, evaluated
+  // speculatively in batches, and the first improvement (in draw order) is
+  // committed -- the generator is rewound to just after it
+  int stall = 0;
+  while (evals < budget && stall < 100000) {
+    std::vector<std::vector<int8_t>> cand;
+    std::vector<uint64_t> state_after;
+    const int B = std::min(threads, budget - evals);
+    while ((int)cand.size() < B && stall < 100000) {
+      int a = (int)rnd((uint64_t)k_free), c = (int)rnd((uint64_t)k_free);
+      if (role(best[a]) == role(best[c])) { stall++; continue; }
+      stall = 0;
+      std::vector<int8_t> pm = best;
+      std::swap(pm[a], pm[c]);
+      cand.push_back(std::move(pm));
+      state_after.push_back(rs);
+    }
+    if (cand.empty()) break;
+    std::vector<double> cost;
+    eval_batch(cand, &cost);
+    for (size_t i = 0; i < cand.size(); i++) {
+      evals++;
+      if (cost[i] < best_c) {
+        best_c = cost[i];
+        best = cand[i];
+        rs = state_after[i];   // later candidates were drawn from the old best
+        break;
+      }
+    }
   }
   bool identity = true;
   for (int v = 0; v < 64; v++) identity &= best[v] == v;

@@ -182,8 +182,10 @@ double model_cost(const Parsed& prog, const KernelSpec& spec);
 // Role search for count mode over an aligned sub-cube of 2^k_free valuations:
 // a permutation of the variables < k_free onto bit positions minimising
 // model_cost (random restarts + swap hill climbing, `budget` evaluations).
-// Returns {} when the identity is best.
-std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& spec, int k_free, int budget, uint64_t seed);
+// Returns {} when the identity is best.  threads > 1 evaluates candidates
+// speculatively in parallel with the same result as threads = 1.
+std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& spec, int k_free, int budget, uint64_t seed,
+                                 int threads = 1);
 
 // CUDA C++ source of one kernel variant (entry point "bfa_kernel").
 std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);

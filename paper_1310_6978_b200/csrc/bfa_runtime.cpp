@@ -40,10 +40,12 @@
 #include "../../include/bfa.h"
 #include "bfa_compiler.hpp"
 #include "bfa_kernels.hpp"
+#include "bfa_sha256.hpp"
 
 namespace {
 
 thread_local std::string g_err;
+thread_local int g_err_code = 0;  // BFA_E_* of the last failing call on this thread
 thread_local std::string g_last_launch = "{}";
 // executed integer cells (LOP3 + IMAD + IMAD operand registers) of the last
 // launch sequence, split by pipe; the bench's roofline numerator
@@ -57,6 +59,12 @@ thread_local uint64_t g_launches = 0;
 thread_local bool g_accumulate = false;
 // inside a fork: nested loops keep their single stream
 thread_local bool g_forked = false;
+// the stream the public call was made on (graph capture runs the work on an
+// internal stream; per-stream state such as work-queue counters keys on this)
+thread_local cudaStream_t g_caller_stream = nullptr;
+// set in worker threads of the library's own host parallelism: nested role
+// searches then run single-threaded instead of oversubscribing the host
+thread_local bool g_worker = false;
 
 // Fork/join of independent launches over side streams (their counts only
 // meet in atomics), so short kernels overlap instead of idling SMs during
@@ -112,6 +120,7 @@ int set_err(int code, const char* fmt, ...) {
   vsnprintf(buf, sizeof buf, fmt, ap);
   va_end(ap);
   g_err = buf;
+  g_err_code = code;
   return code;
 }
 
@@ -210,6 +219,9 @@ uint64_t fnv64(const void* data, size_t n, uint64_t h = 1469598103934665603ull) 
   return h;
 }
 
+const char* const kNvrtcOpts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17"};
+constexpr int kNvrtcOptCount = 3;
+
 int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   if (const char* dir = getenv("BFA_DUMP_SRC")) {  // debugging: keep every generated source
     char path[4096];
@@ -219,8 +231,7 @@ int nvrtc_compile(const std::string& src, std::vector<char>* cubin) {
   nvrtcProgram prog;
   nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "bfa_kernel.cu", 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) return set_err(BFA_E_JIT, "nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-lineinfo", "--std=c++17"};
-  r = nvrtcCompileProgram(prog, 3, opts);
+  r = nvrtcCompileProgram(prog, kNvrtcOptCount, kNvrtcOpts);
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
@@ -282,11 +293,22 @@ void cache_write(const std::string& name, const void* data, size_t n) {
   else remove(t.c_str());
 }
 
-int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin) {
-  char name[64];
-  static const char salt[] = "bfa-cubin-v1|sm_100a|nvrtc-12.9|";
-  snprintf(name, sizeof name, "k_%016llx.cubin",
-           (unsigned long long)fnv64(src.data(), src.size(), fnv64(salt, sizeof salt)));
+// Persistent cache key of a generated source: SHA-256 over a format salt,
+// the NVRTC version, the compile options and the source text.
+std::string cubin_cache_key(const std::string& src) {
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);
+  bfa::Sha256 h;
+  h.update("bfa-cubin-v2|");
+  h.update(std::to_string(major) + "." + std::to_string(minor) + "|");
+  for (int i = 0; i < kNvrtcOptCount; i++) h.update(std::string(kNvrtcOpts[i]) + "|");
+  h.update(src);
+  return h.hex();
+}
+
+int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin, bool use_cache = true) {
+  if (!use_cache) return nvrtc_compile(src, cubin);
+  const std::string name = "k_" + cubin_cache_key(src) + ".cubin";
   if (cache_read(name, cubin)) return BFA_OK;
   int rc = nvrtc_compile(src, cubin);
   if (rc == BFA_OK) cache_write(name, cubin->data(), cubin->size());
@@ -319,6 +341,9 @@ struct Options {
   int queue_inner = 2;           // inner-loop bits of work-queue bodies (-1: inner_bits)
   int queue_role_budget = 400;   // role-search evaluations per work-queue body
   int split_merge = 0;           // > 0: merge sibling leaves of <= this many gates back into their parent
+  int decompose_min_k = 30;      // split_pieces applies to aligned sub-cubes of >= 2^this valuations
+  int split_min_vars = 24;       // pieces with <= this many free variables are not split further
+  int jit_cache = 1;             // 0: this program neither reads nor writes the persistent JIT cache
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -374,7 +399,10 @@ struct bfa_prog {
     uint64_t chunks = 0;
     double bodies_s = 0, nvrtc_s = 0;  // preparation: role searches + emission, NVRTC
     std::vector<uint8_t> queued;  // per piece
-    std::map<int, uint32_t*> ctr; // per device: one self-resetting counter per group
+    // chunk counters, one per group, per (device, caller stream): concurrent
+    // counts of one prepared program on different streams never share a
+    // counter; every call zeroes its counters on its stream first
+    std::map<std::pair<int, uintptr_t>, uint32_t*> ctr;
   };
   std::map<std::string, Queue> queues;
   std::map<std::string, double> decompose_s;  // host seconds per cached decomposition
@@ -414,23 +442,28 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     if (it != p->roles.end()) { spec->perm = it->second; return; }
   }
   // persistent cache: hash of the DAG reachable from the root + the variant
-  static const char salt[] = "bfa-roles-v1|";
-  uint64_t h = fnv64(key.data(), key.size(), fnv64(salt, sizeof salt));
+  bfa::Sha256 h;
+  h.update("bfa-roles-v2|").update(key).update("|");
   for (const bfa::Node& nd : p->parsed.dag.nodes) {
     uint32_t rec[4] = {(uint32_t)nd.kind | ((uint32_t)nd.tt << 8), nd.a, nd.b, nd.val};
-    h = fnv64(rec, sizeof rec, h);
+    h.update(rec, sizeof rec);
   }
-  h = fnv64(&p->parsed.root, sizeof p->parsed.root, h);
-  char name[64];
-  snprintf(name, sizeof name, "r_%016llx.perm", (unsigned long long)h);
+  h.update(&p->parsed.root, sizeof p->parsed.root);
+  const std::string name = "r_" + h.hex() + ".perm";
   std::vector<char> buf;
   std::vector<int8_t> perm;
-  if (cache_read(name, &buf) && (buf.size() == 64 || buf.size() == 1)) {
+  if (p->opt.jit_cache && cache_read(name, &buf) && (buf.size() == 64 || buf.size() == 1)) {
     if (buf.size() == 64) perm.assign(buf.begin(), buf.end());
   } else {
-    perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull);
-    if (perm.empty()) { char z = 0; cache_write(name, &z, 1); }
-    else cache_write(name, perm.data(), perm.size());
+    const int threads = g_worker ? 1 : (int)std::max(1u, std::thread::hardware_concurrency());
+    perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull, threads);
+    if (!p->opt.jit_cache) {
+    } else if (perm.empty()) {
+      char z = 0;
+      cache_write(name, &z, 1);
+    } else {
+      cache_write(name, perm.data(), perm.size());
+    }
   }
   std::lock_guard<std::mutex> lk(p->mu);
   p->roles[key] = perm;
@@ -459,7 +492,7 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
     ne->source = bfa::emit_kernel(p->parsed, spec, &ne->stats);
-    int rc = nvrtc_compile_cached(ne->source, &ne->cubin);
+    int rc = nvrtc_compile_cached(ne->source, &ne->cubin, p->opt.jit_cache);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->jit.find(key);
@@ -502,7 +535,7 @@ int get_kernel_src(const bfa_prog* cp, const std::string& key, const std::string
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
     ne->source = src;
-    int rc = nvrtc_compile_cached(ne->source, &ne->cubin);
+    int rc = nvrtc_compile_cached(ne->source, &ne->cubin, p->opt.jit_cache);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->jit.find(key);
@@ -669,6 +702,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
         th.clear();
         for (size_t i = b0; i < std::min(nseg, b0 + par); i++)
           th.emplace_back([&, i] {
+            g_worker = true;
             rcs[i] = get_kernel_src(p, pkey + "#" + std::to_string(i), plan->sources[i], o.thread_bits, -1, &jes[i],
                                     nullptr);
           });
@@ -792,6 +826,60 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
      << "}";
   g_last_launch = js.str();
   return BFA_OK;
+}
+
+// The specialised count kernel an aligned 2^k_free sub-cube count uses under
+// p's options (the plan's middle segment, roles searched for k_free): its
+// spec, or BFA_E_ARG when the sub-cube runs on the generic kernel only.
+int cube_spec(const bfa_prog* p, int n, int k_free, int sms, bfa::KernelSpec* spec) {
+  const Options& o = p->opt;
+  if (k_free < 5 || k_free > n || o.force_generic || o.engine || o.segment_cells || p->info.luts > 8000)
+    return set_err(BFA_E_ARG, "no specialised count kernel for a 2^%d sub-cube under these options", k_free);
+  const int T = 1 << o.thread_bits;
+  const int full_grid = sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
+  for (const Segment& sg : plan(o, o.slot_bits, n, 0, 1ull << (k_free - 5), full_grid)) {
+    if (sg.generic) continue;
+    spec->mode = bfa::KM_COUNT; spec->generic = false; spec->slot_bits = o.slot_bits;
+    spec->thread_bits = o.thread_bits; spec->inner_bits = sg.m; spec->dual_pipe = o.dual_pipe;
+    spec->imad_cost_pct = o.imad_cost_pct; spec->min_blocks = o.min_blocks;
+    resolve_roles(p, spec, k_free);
+    return BFA_OK;
+  }
+  return set_err(BFA_E_ARG, "no specialised count kernel for a 2^%d sub-cube under these options", k_free);
+}
+
+// Count with exactly the kernel of an aligned 2^k_free sub-cube (same spec,
+// same searched roles, same cubin) over the POSITION range [pos_lo, pos_hi):
+// position q enumerates the valuation mu with mu_v = bit perm[v] of q.
+int count_positions(const bfa_prog* p, int n, int k_free, uint64_t pos_lo, uint64_t pos_hi, uint64_t* count_dev,
+                     cudaStream_t st) {
+  if (!p || !count_dev) return set_err(BFA_E_ARG, "NULL argument");
+  if (n < 5 || n > 63 || p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "bad n=%d", n);
+  int dev;
+  DevInfo di;
+  int rc = current_device(&dev, &di);
+  if (rc) return rc;
+  bfa::KernelSpec spec;
+  if ((rc = cube_spec(p, n, k_free, di.sms, &spec))) return rc;
+  const int ub = spec.slot_bits + spec.thread_bits + spec.inner_bits;  // log2 words per outer iteration
+  const uint64_t unit = 1ull << (ub + 5);
+  if (pos_lo > pos_hi || pos_hi > (1ull << n) || (pos_lo % unit) || (pos_hi % unit))
+    return set_err(BFA_E_ARG, "position range must be multiples of %llu within [0, 2^n)", (unsigned long long)unit);
+  JitEntry* je = nullptr;
+  CUfunction fn;
+  if ((rc = get_kernel(p, spec, dev, &je, &fn))) return rc;
+  cudaError_t ce = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+  if (ce != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(ce));
+  if (pos_hi == pos_lo) return BFA_OK;
+  uint64_t A = pos_lo >> 5, O = (pos_hi - pos_lo) >> (ub + 5), base = 0;
+  uint32_t* o32 = nullptr;
+  uint64_t* cnt = count_dev;
+  uint64_t* mu_out = nullptr;
+  uint64_t cap = 0;
+  const int bps = p->opt.blocks_per_sm ? p->opt.blocks_per_sm : je->occupancy[dev];
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(O, (uint64_t)di.sms * bps));
+  void* args[] = {&A, &O, &base, &o32, &cnt, &mu_out, &cap};
+  return launch(fn, grid, 1 << spec.thread_bits, st, args);
 }
 
 void fill_info(bfa_prog* p) {
@@ -928,7 +1016,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars;
   return k.str();
 }
 
@@ -941,8 +1029,8 @@ int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t
   int dev = 0;
   cudaGetDevice(&dev);
   std::ostringstream k;
-  k << "range|" << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << '|'
-    << options_key(p->opt);
+  k << "range|" << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << '.'
+    << (uintptr_t)g_caller_stream << '|' << options_key(p->opt);
   return with_graph(p, k.str(), st, [&](cudaStream_t s) {
     return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, s, eval, force_roles_k, mu_out, cap);
   });
@@ -988,7 +1076,7 @@ std::vector<std::unique_ptr<bfa_prog>>* ensure_split(const bfa_prog* p, int n, u
     std::vector<std::thread> th;
     std::vector<int> rcs(made.size(), 0);
     for (size_t i = 0; i < made.size(); i++)
-      th.emplace_back([&, i] { rcs[i] = prepare_count(made[i].get(), kk, sms); });
+      th.emplace_back([&, i] { g_worker = true; rcs[i] = prepare_count(made[i].get(), kk, sms); });
     for (auto& t : th) t.join();
     for (int r : rcs)
       if (r) { *rc_out = r; return nullptr; }
@@ -1037,7 +1125,7 @@ int ensure_multi(bfa_prog* mp, const std::string& kkey, std::vector<std::unique_
     {  // role searches in parallel (cached per child and on disk)
       std::vector<std::thread> th;
       for (size_t c = 0; c < live.size(); c++)
-        th.emplace_back([&, c] { resolve_roles(kids[live[c]].get(), &specs[c], kk); });
+        th.emplace_back([&, c] { g_worker = true; resolve_roles(kids[live[c]].get(), &specs[c], kk); });
       for (auto& t : th) t.join();
     }
     bfa_prog::Multi m;
@@ -1096,7 +1184,7 @@ int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, u
       mu_hi <= (1ull << n) && mu_lo < mu_hi && !(mu_lo & 31) && !(mu_hi & 31) && count_dev &&
       p->info.luts <= 8000 && !p->opt.segment_cells) {
     const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
-    if (k >= 30) return decompose_count(p, n, mu_lo, k, count_dev, st);
+    if (k >= p->opt.decompose_min_k) return decompose_count(p, n, mu_lo, k, count_dev, st);
   }
   const int j = p ? p->opt.kernel_cofactor_bits : 0;
   if (!p || eval || mu_out || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
@@ -1185,6 +1273,7 @@ void parallel_for(size_t n, F f) {
   std::vector<std::thread> th;
   for (size_t w = 0; w < W; w++)
     th.emplace_back([&] {
+      g_worker = true;
       for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
     });
   for (auto& t : th) t.join();
@@ -1209,7 +1298,7 @@ static uint64_t piece_work(const bfa_prog* q, int nv) {
 static void score_split(Piece* x) {
   x->split_v = -1;
   x->gain = 0;
-  if (x->work == 0 || x->nv <= 24) return;
+  if (x->work == 0 || x->nv <= x->prog->opt.split_min_vars) return;
   uint64_t total = 0;
   std::vector<int> J = bfa::choose_cofactor_vars(x->prog->parsed, x->nv, 1, &total);
   if (J.empty()) return;
@@ -1251,7 +1340,7 @@ std::vector<std::unique_ptr<bfa_prog>> decompose(const bfa_prog* p, bfa::Parsed 
   std::priority_queue<size_t, std::vector<size_t>, decltype(less)> heap(less);
   auto splittable = [&](size_t i) {
     const Piece& x = pieces[i];
-    return x.work > 0 && x.nv > 24 && (policy == 0 || x.split_v >= 0);
+    return x.work > 0 && x.nv > p->opt.split_min_vars && (policy == 0 || x.split_v >= 0);
   };
   if (splittable(0)) heap.push(0);
   int live = pieces[0].work > 0;
@@ -1435,8 +1524,8 @@ int count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_d
   };
   if (p->opt.graphs) {
     std::ostringstream k;
-    k << "shard|" << dev << '.' << n << '.' << rank << '.' << world << '.' << (uintptr_t)count_dev << '|'
-      << options_key(p->opt);
+    k << "shard|" << dev << '.' << n << '.' << rank << '.' << world << '.' << (uintptr_t)count_dev << '.'
+      << (uintptr_t)g_caller_stream << '|' << options_key(p->opt);
     rc = with_graph(p, k.str(), st, body);
   } else {
     rc = body(st);
@@ -1513,7 +1602,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     uint64_t O = 0;
     int m = 0, nv = 0, s = 0, shift = 0;  // nv: variables the body enumerates (after support reduction)
     double cost = 0, size = 0, cost_o = 0;  // modelled thread-instructions: body, per outer iteration
-    uint64_t hash = 0;
+    std::string hash;                       // SHA-256 of the body source (dedupe key)
     std::unique_ptr<bfa_prog> reduced;      // the support-reduced leaf (null: the leaf itself)
   };
   std::vector<Body> B(elig.size());
@@ -1566,7 +1655,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     b.name = "bfa_body_" + std::to_string(i);
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
     b.src = bfa::emit_kernel(src->parsed, spec, &b.st);
-    b.hash = fnv64(b.src.data(), b.src.size());
+    b.hash = bfa::sha256_hex(b.src);
     b.O = (1ull << (b.nv - 5)) >> (b.s + t + b.m);
     const double inner = b.st.luts_inner + b.st.imads_inner + b.st.derived_inner;
     const double outer = b.st.luts_outer + b.st.imads_outer + b.st.derived_outer;
@@ -1615,7 +1704,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     std::vector<uint64_t> O;
     std::vector<uint32_t> ch;
     bfa_prog::QueueGroup qg;
-    std::map<uint64_t, std::string> seen;  // body hash -> name of its copy in this module
+    std::map<std::string, std::string> seen;  // body SHA-256 -> name of its copy in this module
     for (size_t e : gm) {
       const Body& b = B[e];
       // chunks of ~queue_chunk modelled thread-instructions (65536: ~0.1-0.2
@@ -1689,21 +1778,27 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
   int kernels = 0;
   double l3 = 0, im = 0, decided = 0;
   int rc = BFA_OK;
-  Fork fork(st, dev);
-  if (Q) {
-    uint32_t* ctr = nullptr;
+  // work-queue chunk counters of this (device, caller stream), zeroed on the
+  // launching stream before the fork (a memset node inside a captured
+  // graph): an aborted earlier launch cannot leave a stale chunk number
+  uint32_t* ctr = nullptr;
+  if (Q && !Q->groups.empty()) {
+    const size_t bytes = Q->groups.size() * sizeof(uint32_t);
+    const auto ckey = std::make_pair(dev, (uintptr_t)g_caller_stream);
     {
       std::lock_guard<std::mutex> lk(holder->mu);
-      auto c = Q->ctr.find(dev);
+      auto c = Q->ctr.find(ckey);
       if (c != Q->ctr.end()) ctr = c->second;
     }
-    if (!ctr && !Q->groups.empty()) {
-      const size_t bytes = Q->groups.size() * sizeof(uint32_t);
+    if (!ctr) {
       if (cudaMalloc(&ctr, bytes) != cudaSuccess) return set_err(BFA_E_NOMEM, "queue counters");
-      if (cudaMemset(ctr, 0, bytes) != cudaSuccess) return set_err(BFA_E_CUDA, "queue counters");
       std::lock_guard<std::mutex> lk(holder->mu);
-      Q->ctr[dev] = ctr;
+      Q->ctr[ckey] = ctr;
     }
+    if (cudaMemsetAsync(ctr, 0, bytes, st) != cudaSuccess) return set_err(BFA_E_CUDA, "queue counters");
+  }
+  Fork fork(st, dev);
+  if (Q) {
     const int T = 1 << holder->opt.thread_bits;
 
     std::string regs;
@@ -1768,7 +1863,8 @@ std::vector<std::unique_ptr<bfa_prog>>* get_decomposition(const bfa_prog* p, int
   const uint64_t top_vals = mu_lo & top_mask;
   const std::string key = "split." + std::to_string(n) + "." + std::to_string(k) + "." + std::to_string(top_vals) +
                           "." + std::to_string(p->opt.split_pieces) + "." + std::to_string(p->opt.kernel_cofactor_bits) +
-                          "." + std::to_string(p->opt.split_policy) + "." + std::to_string(p->opt.split_merge);
+                          "." + std::to_string(p->opt.split_policy) + "." + std::to_string(p->opt.split_merge) + "." +
+                          std::to_string(p->opt.split_min_vars);
   *key_out = key;
   {
     std::lock_guard<std::mutex> lk(mp->mu);
@@ -1825,7 +1921,7 @@ int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* c
   uint64_t zero_vals = 0;
   for (auto& q : *kids)
     if (q->info.const_value == 0) { zero++; zero_vals += 1ull << q->piece_nv; }
-  if ((rc = count_pieces(*kids, owner, 0, dev, di.sms, count_dev, st, &kernels, mp, "q." + key))) return rc;
+  if ((rc = count_pieces(*kids, owner, 0, dev, di.sms, count_dev, st, &kernels, mp, "q." + key + "|" + options_key(p->opt)))) return rc;
   std::ostringstream js;
   (void)zero_vals;
   js << "{\"variant\": \"decomposed\", \"pieces\": " << kids->size() << ", \"constant_zero\": " << zero
@@ -1900,6 +1996,13 @@ struct bfa_batch_s {
 extern "C" {
 
 const char* bfa_last_error(void) { return g_err.c_str(); }
+int bfa_last_error_code(void) { return g_err_code; }
+
+int bfa_cache_key(const char* source, char* out, size_t len) {
+  if (!source || !out || len < 65) return set_err(BFA_E_ARG, "NULL argument or buffer < 65 bytes");
+  snprintf(out, len, "%s", cubin_cache_key(source).c_str());
+  return BFA_OK;
+}
 const char* bfa_version(void) { return "bfa 0.1 (sm_100a; NVRTC static)"; }
 
 int bfa_compile(const char* expr, bfa_prog** out) {
@@ -1930,6 +2033,7 @@ int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_v
 
 int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, void* stream) {
   if (!p || !count_dev) return set_err(BFA_E_ARG, "NULL argument");
+  g_caller_stream = (cudaStream_t)stream;
   std::string rep;
   int rc = count_shard(p, n, rank, world, count_dev, (cudaStream_t)stream, &rep);
   if (rc == BFA_OK && !rep.empty()) g_last_launch = rep;
@@ -1957,6 +2061,7 @@ int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint
   if (!mu_out && capacity) return set_err(BFA_E_ARG, "NULL output list");
   if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
   cudaStream_t st = (cudaStream_t)stream;
+  g_caller_stream = st;
   uint64_t dummy_cap = capacity;
   uint64_t* list = mu_out;
   uint64_t* scratch = nullptr;
@@ -2024,6 +2129,9 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_role_budget") { if (v < 1 || v > 100000) return bad(); p->opt.queue_role_budget = (int)v; }
   else if (k == "queue_inner") { if (v < -1 || v > 8) return bad(); p->opt.queue_inner = (int)v; }
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
+  else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
+  else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
+  else if (k == "split_min_vars") { if (v < 5 || v > 63) return bad(); p->opt.split_min_vars = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
   return BFA_OK;
 }
@@ -2045,12 +2153,12 @@ int bfa_prepare(const bfa_prog* p, int n, int sms) {
   }
   const Options& o = p->opt;
   const bool plain = !o.force_generic && !o.engine && !o.segment_cells && p->info.luts <= 8000;
-  if (plain && o.split_pieces > 1 && n >= 30) {
+  if (plain && o.split_pieces > 1 && n >= o.decompose_min_k) {
     std::string key;
     std::vector<std::unique_ptr<bfa_prog>>* kids = get_decomposition(p, n, 0, n, &key);
     std::vector<int> owner(kids->size(), 0);
     bfa_prog::Queue* Q = nullptr;
-    int rc = prepare_pieces(*kids, owner, 0, sms, const_cast<bfa_prog*>(p), "q." + key, &Q);
+    int rc = prepare_pieces(*kids, owner, 0, sms, const_cast<bfa_prog*>(p), "q." + key + "|" + options_key(p->opt), &Q);
     if (rc) return rc;
     bfa_prog* mp = const_cast<bfa_prog*>(p);
     std::ostringstream js;
@@ -2068,12 +2176,37 @@ int bfa_prepare(const bfa_prog* p, int n, int sms) {
   return prepare_count(p, n, sms);
 }
 
+int bfa_roles(const bfa_prog* p, int n, int k_free, int sms, int8_t* perm_out) {
+  if (!p || !perm_out) return set_err(BFA_E_ARG, "NULL argument");
+  if (n < 5 || n > 63 || p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "bad n=%d", n);
+  if (sms <= 0) {
+    int count = 0, dev;
+    DevInfo di;
+    sms = 148;
+    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0 && current_device(&dev, &di) == BFA_OK) sms = di.sms;
+    else cudaGetLastError();
+  }
+  bfa::KernelSpec spec;
+  int rc = cube_spec(p, n, k_free, sms, &spec);
+  if (rc) return rc;
+  for (int v = 0; v < 64; v++) perm_out[v] = v < (int)spec.perm.size() ? spec.perm[v] : (int8_t)v;
+  return BFA_OK;
+}
+
+int bfa_count_positions(const bfa_prog* p, int n, int k_free, uint64_t pos_lo, uint64_t pos_hi, uint64_t* count_dev,
+                        void* stream) {
+  g_caller_stream = (cudaStream_t)stream;
+  return count_positions(p, n, k_free, pos_lo, pos_hi, count_dev, (cudaStream_t)stream);
+}
+
 int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* count_dev, void* stream) {
+  g_caller_stream = (cudaStream_t)stream;
   return run_range(p, n, mu_lo, mu_hi, nullptr, count_dev, (cudaStream_t)stream, false);
 }
 
 int bfa_eval_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
                    uint64_t* count_dev, void* stream) {
+  g_caller_stream = (cudaStream_t)stream;
   return run_range(p, n, mu_lo, mu_hi, out_dev, count_dev, (cudaStream_t)stream, true);
 }
 
@@ -2083,6 +2216,7 @@ uint64_t bfa_count(const bfa_prog* p, int n) {
   if (current_device(&dev, nullptr)) return UINT64_MAX;
   uint64_t* d = nullptr;
   if (scratch_u64(dev, &d)) return UINT64_MAX;
+  g_caller_stream = nullptr;
   if (run_range(p, n, 0, 1ull << n, nullptr, d, nullptr, false)) return UINT64_MAX;
   uint64_t h = 0;
   cudaError_t e = cudaMemcpy(&h, d, sizeof h, cudaMemcpyDeviceToHost);
@@ -2092,6 +2226,7 @@ uint64_t bfa_count(const bfa_prog* p, int n) {
 
 int bfa_eval(const bfa_prog* p, int n, uint64_t* out) {
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  g_caller_stream = nullptr;
   int rc = run_range(p, n, 0, 1ull << n, out, nullptr, nullptr, true);
   if (rc) return rc;
   cudaError_t e = cudaStreamSynchronize(nullptr);
@@ -2113,6 +2248,7 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
   int rc = current_device(&dev, &di);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  g_caller_stream = st;
   std::ostringstream js;
   if (n < 24 || p->opt.force_generic || p->opt.engine || p->opt.segment_cells || p->info.luts > 8000) {
     js << "{\"skipped\": \"problem too small, generic/interpreter engine, or segmented program\"}";
@@ -2169,7 +2305,7 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     std::vector<std::thread> th;
     std::vector<int> rcs(cands.size(), 0);
     for (size_t i = 0; i < cands.size(); i++)
-      if (ok[i]) th.emplace_back([&, i] { JitEntry* e = nullptr;
+      if (ok[i]) th.emplace_back([&, i] { g_worker = true; JitEntry* e = nullptr;
                                           resolve_roles(p, &specs[i], k_free);
                                           rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
                                           if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner; });

@@ -49,6 +49,13 @@ def count_sharded(prog, n: int, group=None, count_range=None, stream=None, balan
         lo, hi = rank_range(n, rank, world)
         t = count_range(n, lo, hi)
     if world > 1:
+        if t.is_cuda:
+            # NCCL orders the collective after torch's CURRENT stream; the
+            # count was produced on `stream`, so make the current stream wait
+            import torch
+            cur = torch.cuda.current_stream(t.device)
+            if stream is not None and stream != cur:
+                cur.wait_stream(stream if not isinstance(stream, int) else torch.cuda.ExternalStream(stream))
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
 

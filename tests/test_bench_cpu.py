@@ -33,7 +33,7 @@ def test_reference_arm_json_line():
     assert d["config"]["n"] == 25 and d["config"]["workload"].startswith("c3_posets")
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"]
-    assert "sub-cube of 2^" in cb["sample"]
+    assert "sub-cube" in cb["sample"] and "of 2^" in cb["sample"] and cb["cpu_model"]
     e2e = d["e2e"]
     assert e2e["value"] == d["value"] and e2e["h2d_bytes_per_step"] == 0 and e2e["d2h_bytes_per_step"] == 0
 

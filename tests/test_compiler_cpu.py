@@ -231,3 +231,41 @@ def test_decomposition_tiles_the_cube():
             "split_policy", policy).set_option("split_merge", merge).shard_plan(n, 1)
     assert sizes[(0, 0)] >= 512 and sizes[(1, 0)] >= 512
     assert sizes[(1, 16)] <= sizes[(1, 0)]
+
+
+def test_cache_key_is_sha256():
+    """The persistent JIT cache key is SHA-256 over salt, NVRTC version,
+    options and source (no 64-bit hash collisions can load a wrong cubin)."""
+    import hashlib
+    src = bfa.Program(W.posets(3)).dump(1, 9)
+    key = bfa.cache_key(src)
+    assert re.fullmatch(r"[0-9a-f]{64}", key)
+    opts = "--gpu-architecture=sm_100a|-lineinfo|--std=c++17|"
+    expect = hashlib.sha256(("bfa-cubin-v2|12.9|" + opts + src).encode()).hexdigest()
+    assert key == expect
+    assert bfa.cache_key(src + " ") != key
+
+
+def test_last_error_code():
+    """bfa_last_error_code classifies failures (no message parsing)."""
+    with pytest.raises(bfa.BfaError) as e:
+        bfa.Program("x0 &")
+    assert e.value.code == bfa.BFA_E_PARSE == bfa._load().bfa_last_error_code()
+    with pytest.raises(bfa.BfaError):
+        bfa.Program("x0").set_option("slot_bits", 9)
+    assert bfa._load().bfa_last_error_code() == bfa.BFA_E_ARG
+
+
+def test_roles_are_a_permutation_of_the_free_variables():
+    """bfa_roles (host only): the count kernel of an aligned 2^k sub-cube
+    enumerates it in a permuted variable order that fixes every variable
+    >= k; the same program object reports the same order again."""
+    text, n, _ = W.config("c4")
+    p = bfa.Program(text).set_option("slot_bits", 5).set_option("imad_cost_pct", 50)
+    for k in (36, 30):
+        perm = p.roles(n, k, sms=148)
+        assert sorted(perm) == list(range(64))
+        assert all(perm[v] == v for v in range(k, 64))
+        assert p.roles(n, k, sms=148) == perm
+    with pytest.raises(bfa.BfaError):
+        bfa.Program(text).set_option("force_generic", 1).roles(n, n, sms=148)

@@ -1,6 +1,8 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit
 for bit.  Vectors and counts are integer results, so the bar is exact
 equality (BASELINE.json north star: "bit-exact")."""
+import re
+
 import numpy as np
 import pytest
 import torch
@@ -11,6 +13,7 @@ import workloads as W
 pytestmark = pytest.mark.gpu
 
 bfa = pytest.importorskip("paper_1310_6978_b200")
+from paper_1310_6978_b200 import presets  # noqa: E402
 
 
 def host(words_t):
@@ -199,23 +202,66 @@ def test_c4_full_set_bits():
     assert np.array_equal(gbits, obits)
 
 
-def test_c5_bench_config_subcubes():
-    """Config C5 (n=42 random DAG), the bench workload, in the bench's launch
-    configuration: full count, invariant with ~f, and oracle sub-cube counts
-    (top 22 ids fixed; P-13)."""
-    text, n, _ = W.config("c5")
-    p = bfa.Program(text)
-    c = p.count(n)
-    body = "\n".join(text.splitlines()[:-1])
-    out = text.splitlines()[-1]
-    assert c + bfa.Program(f"{body}\n~{out}").count(n) == 1 << n
-    rng = np.random.default_rng(11)
+def renamed(text, perm):
+    """f'(x) = f(x with x_v renamed x_perm[v]) -- input transformation only
+    (the oracle's arithmetic is untouched): the models of f' at position q are
+    the models of f at the valuation the permuted kernel enumerates at q."""
+    return re.sub(r"\bx(\d+)\b", lambda m: f"x{perm[int(m.group(1))]}", text)
+
+
+@pytest.mark.parametrize("cfg", ["c5", "c4"])
+def test_exhaustive_bench_kernel_vs_oracle(cfg):
+    """The headline kernel bench.py times (presets.EXHAUSTIVE over the whole
+    2^n cube: same variant, same searched roles, same cubin) against the
+    oracle on 4 random sub-ranges of its enumeration order, 2^24 valuations
+    each (P-13; C5 cannot be oracle-checked whole).  bfa_count_positions runs
+    exactly that kernel; the oracle counts the renamed program f' on the same
+    position range."""
+    text, n, expect = W.config(cfg)
+    p = presets.apply(bfa.Program(text), presets.EXHAUSTIVE)
+    perm = p.roles(n)
+    assert sorted(perm) == list(range(64)) and perm != list(range(64))
+    text2 = renamed(text, perm)
+    rng = np.random.default_rng(13106978)
     for _ in range(4):
-        lo = int(rng.integers(0, 1 << 22)) << 20
-        hi = lo + (1 << 20)
-        assert int(p.count_range(n, lo, hi).item()) == oracle.count(text, n, lo, hi)
-        ow, _ = oracle.evaluate(text, n, lo, lo + (1 << 16))
-        assert np.array_equal(host(p.eval_range(n, lo, lo + (1 << 16))), ow)
+        if cfg == "c4":          # sub-ranges where every reflexivity letter is 1 (else no models)
+            lo = (int(rng.integers(0, 1 << 36)) | sum(1 << perm[35 - 7 * i] for i in range(6))) & ~((1 << 24) - 1)
+        else:
+            lo = int(rng.integers(0, 1 << (n - 24))) << 24
+        got = int(p.count_positions(n, n, lo, lo + (1 << 24)).item())
+        assert got == oracle.count(text2, n, lo, lo + (1 << 24)), (cfg, lo)
+    # the same compiled kernel over the whole cube: the count bench.py reports
+    c = p.count(n)
+    ll = bfa.last_launch()
+    assert ll["kernels"] == 1 and ll["segments"][0]["roles"] == "searched" and ll["segments"][0]["s"] == 5
+    if expect is not None:
+        assert c == expect
+    else:                          # C5: complement invariant (P-11) with the same preset
+        body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+        pc = presets.apply(bfa.Program(f"{body}\n~{out}"), presets.EXHAUSTIVE)
+        assert c + pc.count(n) == 1 << n
+
+
+def test_decomposed_work_queue_vs_oracle():
+    """The decomposed path (presets.DECOMPOSED: Shannon leaves in persistent
+    work-queue kernels, queue_inner 2, role budget 400, slot 5, IMAD 50),
+    scaled down so it runs on oracle-checkable sub-cubes: decomposition of
+    aligned 2^24 C5 sub-cubes (decompose_min_k 24) into leaves of >= 18
+    variables (split_min_vars 18), one module and many modules, direct /
+    graph-captured / replayed calls, each against the oracle."""
+    text, n, _ = W.config("c5")
+    rng = np.random.default_rng(42)
+    for qb in (512, 4, 512, 4):
+        p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=64, queue_bodies=qb,
+                          decompose_min_k=24, split_min_vars=18)
+        lo = int(rng.integers(0, 1 << (n - 24))) << 24
+        expect = oracle.count(text, n, lo, lo + (1 << 24))
+        out = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for _ in range(3):                       # direct, capture, replay
+            p.count_range(n, lo, lo + (1 << 24), out=out)
+            assert int(out.item()) == expect, (qb, lo)
+        ll = bfa.last_launch()
+        assert ll["variant"] == "decomposed" and ll["queue"]["bodies"] > 1, ll
 
 
 def test_role_search_subcubes():
@@ -375,19 +421,58 @@ def test_graph_replay():
 
 def test_count_shard_sums_to_count():
     """Work-balanced cofactor sharding (bfa_count_shard): the ranks' shares,
-    computed here one after another in one process, sum to the full count for
-    P = 2, 4, 8; the LPT loads are balanced."""
-    for cfg in ("c4", "c5"):
-        text, n, _ = W.config(cfg)
-        full = bfa.Program(text).count(n)
-        p = bfa.Program(text)
-        for world in (2, 4, 8):
-            out = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
-            for rep in range(3):          # direct, graph capture, graph replay
-                shares = [int(p.count_shard(n, r, world, out=out[r]).item()) for r in range(world)]
-                assert sum(shares) == full, (cfg, world, rep, shares)
-            load = bfa.last_launch()["load"]
-            assert len(load) == world and max(load) <= 1.6 * sum(load) / world, (cfg, world, load)
+    computed here one after another in one process, sum to the closed form
+    A001035(6) = 130023 on C4, and on C5 the shares of f and of ~f sum to
+    2^42 (P-11) for P = 2, 4, 8; the LPT loads are balanced."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text)
+    for world in (2, 4, 8):
+        out = [torch.zeros(1, dtype=torch.int64, device="cuda") for _ in range(world)]
+        for rep in range(3):          # direct, graph capture, graph replay
+            shares = [int(p.count_shard(n, r, world, out=out[r]).item()) for r in range(world)]
+            assert sum(shares) == expect, (world, rep, shares)
+        load = bfa.last_launch()["load"]
+        assert len(load) == world and max(load) <= 1.6 * sum(load) / world, (world, load)
+    text, n, _ = W.config("c5")
+    body, outl = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
+    p, pc = bfa.Program(text), bfa.Program(f"{body}\n~{outl}")
+    for world in (2, 4, 8):
+        a = sum(int(p.count_shard(n, r, world).item()) for r in range(world))
+        b = sum(int(pc.count_shard(n, r, world).item()) for r in range(world))
+        assert a + b == 1 << n, world
+
+
+def test_concurrent_counts_on_two_streams():
+    """One prepared decomposed C5 program counted on two streams at once
+    (work-queue chunk counters are per caller stream and zeroed by every
+    call): every result is exact, over direct, captured and replayed calls."""
+    text, n, _ = W.config("c5")
+    p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=1024, queue_bodies=64)
+    ref = torch.zeros(1, dtype=torch.int64, device="cuda")
+    p.count_range(n, 0, 1 << n, out=ref)
+    expect = int(ref.item())
+    assert expect == presets.apply(bfa.Program(text), presets.EXHAUSTIVE).count(n)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    o1 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    o2 = torch.zeros(4, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    for i in range(4):
+        p.count_range(n, 0, 1 << n, out=o1[i:i + 1], stream=s1)
+        p.count_range(n, 0, 1 << n, out=o2[i:i + 1], stream=s2)
+    torch.cuda.synchronize()
+    assert o1.tolist() == [expect] * 4 and o2.tolist() == [expect] * 4
+
+
+def test_queue_options_change_rebuilds():
+    """Changing a launch option after a work-queue count rebuilds the
+    modules (the queue key covers every option): thread_bits 8 -> 7 keeps
+    the count exact."""
+    text, n, expect = W.config("c4")
+    p = bfa.Program(text).set_option("split_pieces", 256).set_option("queue_bodies", 32)
+    assert p.count(n) == expect
+    p.set_option("thread_bits", 7)
+    assert p.count(n) == expect
+    assert p.count(n) == expect
 
 
 def test_autotune_keeps_results():
