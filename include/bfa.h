@@ -193,6 +193,14 @@ int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
  * sub-cube would run on the generic kernel (no roles). */
 int bfa_roles(const bfa_prog* p, int n, int k_free, int sms, int8_t* perm_out);
 
+/* Host-only preparation of the count kernel for aligned 2^k_free sub-cubes
+ * (e.g. one rank's cofactor range, k_free = n - log2 P): role search + NVRTC,
+ * results cached in p and in the persistent JIT cache, so other processes
+ * (the other ranks) load them instead of re-deriving them.  No device needed
+ * (sms <= 0: the current device's, else 148).  BFA_E_ARG when such a count
+ * would run on the generic kernel only. */
+int bfa_prepare_range(const bfa_prog* p, int n, int k_free, int sms);
+
 /* Count with EXACTLY the kernel (same variant, roles and cubin) that a count
  * of an aligned 2^k_free sub-cube launches, over the position range
  * [pos_lo, pos_hi) of its enumeration order: the number of q in the range
@@ -221,6 +229,14 @@ int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* cou
  * rank computes the same plan. */
 int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_vars, uint64_t* work, int capacity,
                    int* n_pieces);
+
+/* Piece `index` of that plan as program text (grammar above; host only): its
+ * reduced program over its piece_vars free variables, renumbered 0.. in
+ * increasing order of the original ids (as bfa_assume does).  Its model count
+ * over 2^piece_vars valuations is the piece's share of bfa_count(p, n), so an
+ * independent evaluator (the CPU oracle) can check a rank's share piece by
+ * piece.  Returns the text length (excluding NUL), writing up to len bytes. */
+int64_t bfa_shard_piece_text(const bfa_prog* p, int n, int world, int index, char* buf, size_t len);
 
 /* Host-only preparation (SURVEY.md §8(b) bfa_compile's JIT, ahead of time):
  * everything bfa_count(p, n) compiles before its first launch -- the
@@ -315,6 +331,8 @@ int bfa_last_launch_json(char* buf, size_t len);
  * what = 4: CUDA source of the fused materialised-mode kernel.
  * what = 5: JSON summary of the segmented-execution plan (large programs).
  * what = 6: CUDA source of segment n of that plan.
+ * what = 7: the reduced program (hash-consed DAG after the Reduction) as
+ *           text in the grammar above: one `let` per gate, then the root.
  * Returns the full length needed (excluding NUL) or a negative error. */
 int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len);
 

@@ -54,6 +54,8 @@ _SIGS = {
     "bfa_shard_plan": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.POINTER(_c.c_int), _c.POINTER(_c.c_int),
                                   _c.POINTER(_c.c_uint64), _c.c_int, _c.POINTER(_c.c_int)]),
     "bfa_prepare": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int]),
+    "bfa_prepare_range": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int]),
+    "bfa_shard_piece_text": (_c.c_int64, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.c_char_p, _c.c_size_t]),
     "bfa_roles": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_int, _c.POINTER(_c.c_int8)]),
     "bfa_count_positions": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p,
                                        _c.c_void_p]),
@@ -204,6 +206,12 @@ class Program:
         _check(_load().bfa_prepare(self._h, n, sms))
         return self
 
+    def prepare_range(self, n: int, k_free: int, sms: int = 0):
+        """bfa_prepare_range (host only): compile the count kernel for aligned
+        2^k_free sub-cubes (a rank's cofactor range); returns self."""
+        _check(_load().bfa_prepare_range(self._h, n, k_free, sms))
+        return self
+
     def count_shard(self, n: int, rank: int, world: int, out=None, stream=None):
         """bfa_count_shard: this rank's share of the count under work-balanced
         cofactor sharding (sum over ranks = count(n))."""
@@ -220,6 +228,15 @@ class Program:
         own, nv, wk = (ctypes.c_int * k)(), (ctypes.c_int * k)(), (ctypes.c_uint64 * k)()
         _check(lib.bfa_shard_plan(self._h, n, world, own, nv, wk, k, ctypes.byref(np_)))
         return [(own[i], nv[i], wk[i]) for i in range(k)]
+
+    def shard_piece_text(self, n: int, world: int, index: int) -> str:
+        """bfa_shard_piece_text (host only): piece `index` of the shard plan
+        as program text over its free variables."""
+        lib = _load()
+        size = _check(lib.bfa_shard_piece_text(self._h, n, world, index, None, 0))
+        buf = ctypes.create_string_buffer(size + 1)
+        _check(lib.bfa_shard_piece_text(self._h, n, world, index, buf, size + 1))
+        return buf.value.decode()
 
     def eval(self, n: int, out=None):
         """bfa_eval: the full-DNF vector as words_for(n) device int64 words (synchronous)."""

@@ -1517,6 +1517,53 @@ InterpProgram build_interp(const Parsed& prog) {
   return ip;
 }
 
+std::string to_text(const Parsed& prog) {
+  // the cone of the root in node order (inputs precede their gates)
+  const Dag& d = prog.dag;
+  std::vector<uint8_t> in_cone(d.nodes.size(), 0);
+  std::vector<uint32_t> st{lit_node(prog.root)};
+  while (!st.empty()) {
+    const uint32_t k = st.back();
+    st.pop_back();
+    if (in_cone[k]) continue;
+    in_cone[k] = 1;
+    if (d.nodes[k].kind == NK_GATE) { st.push_back(d.nodes[k].a); st.push_back(d.nodes[k].b); }
+  }
+  auto name = [&](uint32_t k) -> std::string {
+    const Node& nd = d.nodes[k];
+    if (nd.kind == NK_VAR) return "x" + std::to_string(nd.val);
+    if (nd.kind == NK_CONST) return "0";
+    return "g" + std::to_string(k);
+  };
+  std::ostringstream os;
+  for (size_t k = 0; k < d.nodes.size(); k++) {
+    if (!in_cone[k] || d.nodes[k].kind != NK_GATE) continue;
+    const Node& nd = d.nodes[k];
+    const std::string a = name(nd.a), b = name(nd.b);
+    std::string e;
+    switch (nd.tt) {   // bit (a + 2b) = f(a, b); f(0, 0) = 0 after normalisation
+      case 0x2: e = a + " & ~" + b; break;
+      case 0x4: e = "~" + a + " & " + b; break;
+      case 0x6: e = a + " ^ " + b; break;
+      case 0x8: e = a + " & " + b; break;
+      case 0xE: e = a + " | " + b; break;
+      default: {
+        std::string t;
+        for (int m = 0; m < 4; m++)
+          if ((nd.tt >> m) & 1)
+            t += (t.empty() ? "" : " | ") + std::string("(") + ((m & 1) ? "" : "~") + a + " & " + ((m & 2) ? "" : "~") +
+                 b + ")";
+        e = t.empty() ? "0" : t;
+      }
+    }
+    os << "let " << name((uint32_t)k) << " = " << e << "\n";
+  }
+  const Node& rn = d.nodes[lit_node(prog.root)];
+  if (rn.kind == NK_CONST) os << (lit_neg(prog.root) ? "1" : "0") << "\n";
+  else os << (lit_neg(prog.root) ? "~" : "") << name(lit_node(prog.root)) << "\n";
+  return os.str();
+}
+
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts) {
   Dag D;
   std::vector<Lit> subst(64);

@@ -232,4 +232,9 @@ std::string emit_batch(const std::vector<const Parsed*>& progs, int thread_bits)
 // LUT cover IR text (bfa_dump what=0) and the plain cover size L.
 std::string dump_ir(const Parsed& prog, uint32_t* n_luts);
 
+// The program's reduced DAG as text in the grammar of include/bfa.h: one
+// `let gK = ...` per gate of the root's cone, then the root as the single
+// constraint (0 / 1 for a constant program).
+std::string to_text(const Parsed& prog);
+
 }  // namespace bfa

@@ -2031,6 +2031,18 @@ int bfa_shard_plan(const bfa_prog* p, int n, int world, int* owner, int* piece_v
   return BFA_OK;
 }
 
+int64_t bfa_shard_piece_text(const bfa_prog* p, int n, int world, int index, char* buf, size_t len) {
+  if (!p) return set_err(BFA_E_ARG, "NULL argument");
+  ShardPlan plan;
+  int rc = shard_plan(p, n, world, &plan);
+  if (rc) return rc;
+  if (index < 0 || index >= (int)plan.kids->size())
+    return set_err(BFA_E_ARG, "piece %d of %zu", index, plan.kids->size());
+  const std::string s = bfa::to_text((*plan.kids)[index]->parsed);
+  if (buf && len) snprintf(buf, len, "%s", s.c_str());
+  return (int64_t)s.size();
+}
+
 int bfa_count_shard(const bfa_prog* p, int n, int rank, int world, uint64_t* count_dev, void* stream) {
   if (!p || !count_dev) return set_err(BFA_E_ARG, "NULL argument");
   g_caller_stream = (cudaStream_t)stream;
@@ -2191,6 +2203,22 @@ int bfa_roles(const bfa_prog* p, int n, int k_free, int sms, int8_t* perm_out) {
   if (rc) return rc;
   for (int v = 0; v < 64; v++) perm_out[v] = v < (int)spec.perm.size() ? spec.perm[v] : (int8_t)v;
   return BFA_OK;
+}
+
+int bfa_prepare_range(const bfa_prog* p, int n, int k_free, int sms) {
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
+  if (n < 5 || n > 63 || p->info.max_var_id >= n) return set_err(BFA_E_RANGE, "bad n=%d", n);
+  if (sms <= 0) {
+    int count = 0, dev;
+    DevInfo di;
+    sms = 148;
+    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0 && current_device(&dev, &di) == BFA_OK) sms = di.sms;
+    else cudaGetLastError();
+  }
+  bfa::KernelSpec spec;
+  int rc = cube_spec(p, n, k_free, sms, &spec);
+  if (rc) return rc;
+  return get_kernel(p, spec, -1, nullptr, nullptr);
 }
 
 int bfa_count_positions(const bfa_prog* p, int n, int k_free, uint64_t pos_lo, uint64_t pos_hi, uint64_t* count_dev,
@@ -2747,6 +2775,8 @@ int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
   std::string s;
   if (what == 0) {
     s = bfa::dump_ir(p->parsed, nullptr);
+  } else if (what == 7) {
+    s = bfa::to_text(p->parsed);
   } else if (what == 5 || what == 6) {
     // 5: segmented-execution plan summary (JSON); 6: source of segment n
     const int seg = p->opt.segment_cells ? p->opt.segment_cells : 768;

@@ -161,7 +161,7 @@ def test_invariants_large():
 
 # ------------------------------------------------------------ configs at full size
 def test_c4_posets6_count_and_subcubes():
-    """Config C4 at full size (n=36) in the bench launch configuration:
+    """Config C4 at full size (n=36) with the default options:
     count = A001035(6) = 130023; sampled cofactor sub-cubes of the vector
     equal the oracle's."""
     text, n, expect = W.config("c4")
@@ -251,10 +251,21 @@ def test_decomposed_work_queue_vs_oracle():
     graph-captured / replayed calls, each against the oracle."""
     text, n, _ = W.config("c5")
     rng = np.random.default_rng(42)
+    base = bfa.Program(text)
+
+    def nontrivial_subcube():
+        # a sub-cube whose cofactor (top 18 variables fixed) the Reduction
+        # does not fold to a constant, so it really decomposes
+        while True:
+            lo = int(rng.integers(0, 1 << (n - 24))) << 24
+            q, _, _ = base.assume(n, {v: (lo >> v) & 1 for v in range(24, n)})
+            if q.info["const_value"] == -1 and q.info["gates"] >= 100:
+                return lo
+
     for qb in (512, 4, 512, 4):
         p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=64, queue_bodies=qb,
                           decompose_min_k=24, split_min_vars=18)
-        lo = int(rng.integers(0, 1 << (n - 24))) << 24
+        lo = nontrivial_subcube()
         expect = oracle.count(text, n, lo, lo + (1 << 24))
         out = torch.zeros(1, dtype=torch.int64, device="cuda")
         for _ in range(3):                       # direct, capture, replay
