@@ -132,7 +132,7 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "queue_inner"   inner-loop bits of work-queue bodies (default 2; -1:
  *                   inner_bits)
  *   "queue_role_budget" role-search evaluations per work-queue body
- *                   (default 400)
+ *                   (default 100)
  *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
  *                   leaves of <= this many gates each back into their parent
  *                   (default 0)
@@ -325,7 +325,8 @@ int bfa_last_launch_json(char* buf, size_t len);
 /* what = 0: LUT3 cover IR text, one line per LUT:
  *           "L<k> = lop3(<a>, <b>, <c>, 0x<imm>)" with operands "x<id>",
  *           "L<j>" or "0x<word>", followed by "out = [~]<operand>".
- * what = 1: CUDA source of the specialised count kernel for n.
+ * what = 1: source of the specialised count kernel for n: PTX (option "ptx",
+ *           the default) or CUDA C++ (ptx = 0).
  * what = 2: CUDA source of the specialised eval kernel for n.
  * what = 3: CUDA source of the unspecialised (generic) count kernel.
  * what = 4: CUDA source of the fused materialised-mode kernel.
@@ -350,8 +351,9 @@ int bfa_last_error_code(void);
 const char* bfa_version(void);
 
 /* Persistent JIT cache key of a generated kernel source (host only): the
- * 64-hex-digit SHA-256 over the cache format salt, the NVRTC version, the
- * NVRTC options and the source; cubins are stored as k_<key>.cubin under
+ * 64-hex-digit SHA-256 over the cache format salt, the compiler version
+ * (NVRTC for CUDA C++, the PTX compiler for generated PTX), its options and
+ * the source; cubins are stored as k_<key>.cubin under
  * $BFA_JIT_CACHE (default ~/.cache/bfa_jit; "0" disables the cache).  out
  * receives 64 digits + NUL (len >= 65), else BFA_E_ARG. */
 int bfa_cache_key(const char* source, char* out, size_t len);

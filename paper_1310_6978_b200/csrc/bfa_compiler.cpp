@@ -526,8 +526,12 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
   }
   std::vector<ImadOpt> imad(N);
   std::vector<uint8_t> use_imad(N, 0);
-  const int kMaxCuts = 8;
-  std::vector<std::vector<Cut>> cuts(N);
+  // cut sets in one flat array: <= kMaxCuts priority cuts + the trivial cut
+  // per node (no per-node allocation: map_luts runs inside the role search)
+  constexpr int kMaxCuts = 8, kSlots = kMaxCuts + 1;
+  std::vector<Cut> cutbuf(N * kSlots);
+  std::vector<uint8_t> ncut(N, 0);
+  auto cuts_of = [&](size_t k) { return &cutbuf[k * kSlots]; };
   std::vector<float> af(N, 0.f);
   auto leaf_share = [&](uint32_t l) -> float {
     return dag.nodes[l].kind == NK_GATE ? af[l] / (float)std::max<uint32_t>(1, fanout[l]) : 0.f;
@@ -536,10 +540,15 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
     if (!in_cone[n]) continue;
     const Node& nd = dag.nodes[n];
     Cut triv{{(uint32_t)n, 0, 0}, 1, 0xF0, 0.f};
-    if (nd.kind != NK_GATE) { cuts[n].push_back(triv); continue; }
-    std::vector<Cut> cand;
-    for (const Cut& ca : cuts[nd.a]) {
-      for (const Cut& cb : cuts[nd.b]) {
+    if (nd.kind != NK_GATE) { cuts_of(n)[0] = triv; ncut[n] = 1; continue; }
+    Cut cand[kSlots * kSlots];
+    int nc = 0;
+    const Cut* CA = cuts_of(nd.a);
+    const Cut* CB = cuts_of(nd.b);
+    for (int ia = 0; ia < ncut[nd.a]; ia++) {
+      const Cut& ca = CA[ia];
+      for (int ib = 0; ib < ncut[nd.b]; ib++) {
+        const Cut& cb = CB[ib];
         uint32_t L[6]; int nl = 0;
         for (int j = 0; j < ca.n; j++) L[nl++] = ca.leaf[j];
         for (int j = 0; j < cb.n; j++) {
@@ -562,17 +571,17 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
         for (int q = 0; q < nl; q++) cost += leaf_share(L[q]);
         c.cost = cost;
         bool dup = false;
-        for (const Cut& e : cand)
-          if (e.n == c.n && std::equal(e.leaf, e.leaf + e.n, c.leaf)) { dup = true; break; }
-        if (!dup) cand.push_back(c);
+        for (int e = 0; e < nc && !dup; e++)
+          dup = cand[e].n == c.n && std::equal(cand[e].leaf, cand[e].leaf + c.n, c.leaf);
+        if (!dup) cand[nc++] = c;
       }
     }
-    std::stable_sort(cand.begin(), cand.end(), [](const Cut& x, const Cut& y) {
+    std::stable_sort(cand, cand + nc, [](const Cut& x, const Cut& y) {
       if (x.cost != y.cost) return x.cost < y.cost;
       return x.n < y.n;
     });
-    if ((int)cand.size() > kMaxCuts) cand.resize(kMaxCuts);
-    af[n] = cand.empty() ? (float)weights[res.node_level[n]] : cand[0].cost;
+    nc = std::min(nc, kMaxCuts);
+    af[n] = nc == 0 ? (float)weights[res.node_level[n]] : cand[0].cost;
     // IMAD cell: u ? f1(x) : f0(x) for a word-uniform input u
     if (imad_cost > 0 && (uniform[nd.a] || uniform[nd.b])) {
       ImadOpt o;
@@ -593,8 +602,9 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
       float c = (float)(weights[res.node_level[n]] * imad_cost) + leaf_share(o.x) + leaf_share(o.u);
       if (c < af[n]) { af[n] = c; use_imad[n] = 1; }
     }
-    cuts[n] = cand;
-    cuts[n].push_back(triv);
+    std::copy(cand, cand + nc, cuts_of(n));
+    cuts_of(n)[nc] = triv;
+    ncut[n] = (uint8_t)(nc + 1);
   }
   // cover extraction from the outputs (reverse topological order)
   std::vector<uint8_t> req(N, 0);
@@ -614,7 +624,7 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
       req[o.x] = 1; req[o.u] = 1;
       continue;
     }
-    const Cut& c = cuts[k][0];
+    const Cut& c = cuts_of(k)[0];
     Lut lut{};
     lut.root = (uint32_t)k;
     lut.nin = c.n;
@@ -840,13 +850,31 @@ static void build_specialised(const Parsed& prog, const KernelSpec& spec, Built*
 // measures 18.5 T LOP3/s, 18.5 T IMAD/s and 35.2 T/s for a 1:1 mix).
 static double model_time(const Built& b, const MapResult& r, const KernelSpec& spec) {
   double A = 0, F = 0;
-  std::ostringstream sink;
-  Emitter probe(b.D, sink);
+  // IMAD operand registers u * k + c, one per distinct (u, k, c) (as
+  // Emitter::plan_cell records them), computed at u's loop level
+  std::vector<uint64_t> derived;
+  auto note = [&](uint32_t u, int k, int c) {
+    if (k == 0 || (k == 1 && c == 0)) return;
+    derived.push_back((uint64_t)u << 16 | (uint64_t)(k + 8) << 8 | (uint64_t)(c + 8));
+  };
   for (const Lut& L : r.luts) {
-    if (L.kind == 1) { F += b.w[L.level]; probe.plan_cell(L); }
-    else A += b.w[L.level];
+    if (L.kind != 1) { A += b.w[L.level]; continue; }
+    F += b.w[L.level];
+    if (b.D.nodes[L.in[0]].kind == NK_CONST) continue;
+    int m0, c0, m1, c1;
+    Emitter::mc(L.f0, &m0, &c0);
+    Emitter::mc(L.f1, &m1, &c1);
+    note(L.in[1], m0 - m1, m0);
+    note(L.in[1], c0 - c1, c0);
   }
-  for (auto& kv : probe.derived) F += b.w[r.node_level[kv.first]] * (double)kv.second.size();
+  std::sort(derived.begin(), derived.end());
+  derived.erase(std::unique(derived.begin(), derived.end()), derived.end());
+  for (size_t i = 0; i < derived.size();) {   // per u: w(level of u) x its distinct (k, c)
+    size_t j = i;
+    while (j < derived.size() && (derived[j] >> 16) == (derived[i] >> 16)) j++;
+    F += b.w[r.node_level[(uint32_t)(derived[i] >> 16)]] * (double)(j - i);
+    i = j;
+  }
   const double other = spec.generic ? 4.0 : b.S + b.S / 2.0 + 2.0 + 2.0 * b.m;
   return std::max({2 * (A + other), 2 * F, A + F + other});
 }
@@ -914,6 +942,58 @@ double model_cost(const Parsed& prog, const KernelSpec& spec) {
   return t;
 }
 
+// Constructive start of the role search: slot positions to the variables
+// whose joint cofactors reduce the program most; the others ranked by forward
+// cone size (gates that depend on the variable), largest first, to the lane,
+// thread and outer positions; the smallest cones (variables outside the
+// support first) take the inner-loop positions, so most cells hoist out of
+// the inner loop.
+static std::vector<int8_t> constructive_roles(const Parsed& prog, const KernelSpec& spec, int k_free) {
+  const int s = spec.slot_bits, t = spec.thread_bits, m = spec.inner_bits;
+  std::vector<int8_t> pm(64);
+  for (int v = 0; v < 64; v++) pm[v] = (int8_t)v;
+  std::vector<int> slot = choose_cofactor_vars(prog, k_free, std::max(0, std::min(s, k_free - 5)));
+  const Dag& d = prog.dag;
+  std::vector<uint64_t> sup(d.nodes.size(), 0);
+  std::vector<uint8_t> in_cone(d.nodes.size(), 0);
+  std::vector<uint32_t> st{lit_node(prog.root)};
+  while (!st.empty()) {
+    const uint32_t k = st.back();
+    st.pop_back();
+    if (in_cone[k]) continue;
+    in_cone[k] = 1;
+    if (d.nodes[k].kind == NK_GATE) { st.push_back(d.nodes[k].a); st.push_back(d.nodes[k].b); }
+  }
+  std::vector<uint32_t> cone(64, 0);
+  for (size_t k = 0; k < d.nodes.size(); k++) {
+    const Node& nd = d.nodes[k];
+    if (nd.kind == NK_VAR) {
+      sup[k] = 1ull << nd.val;
+    } else if (nd.kind == NK_GATE) {
+      sup[k] = sup[nd.a] | sup[nd.b];
+      if (in_cone[k])
+        for (uint64_t b = sup[k]; b; b &= b - 1) cone[__builtin_ctzll(b)]++;
+    }
+  }
+  std::vector<int> rest;
+  for (int v = 0; v < k_free; v++)
+    if (std::find(slot.begin(), slot.end(), v) == slot.end()) rest.push_back(v);
+  std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return cone[x] > cone[y]; });
+  std::vector<int> pos_order;  // positions in the order the ranked variables take them
+  for (int q = 0; q < std::min(5, k_free); q++) pos_order.push_back(q);                     // lanes
+  for (int q = 5 + s; q < std::min(k_free, 5 + s + t); q++) pos_order.push_back(q);         // thread
+  for (int q = k_free - 1; q >= 5 + s + t + m; q--) pos_order.push_back(q);                 // outer
+  for (int q = 5 + s + t; q < std::min(k_free, 5 + s + t + m); q++) pos_order.push_back(q); // inner
+  std::vector<uint8_t> taken(64, 0);
+  for (size_t i = 0; i < slot.size(); i++) { pm[slot[i]] = (int8_t)(5 + i); taken[5 + i] = 1; }
+  size_t r = 0;
+  for (int q : pos_order)
+    if (!taken[q] && r < rest.size()) { pm[rest[r++]] = (int8_t)q; taken[q] = 1; }
+  for (int q = 0; q < k_free && r < rest.size(); q++)  // fewer slot variables than slots
+    if (!taken[q]) { pm[rest[r++]] = (int8_t)q; taken[q] = 1; }
+  return pm;
+}
+
 std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int k_free, int budget, uint64_t seed,
                                  int threads) {
   // Count mode over an aligned sub-cube of 2^k_free valuations: any
@@ -921,16 +1001,19 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
   // so the count is unchanged; search the one whose cover is cheapest.
   //
   // The search is a fixed sequence of candidates drawn from one seeded
-  // generator (random restarts, then swap hill climbing); with threads > 1
-  // the model evaluations of consecutive candidates run speculatively in
-  // parallel and are committed in sequence order, so the result is the same
-  // for every thread count (and on every machine).
+  // generator: the constructive start, random restarts, then swap hill
+  // climbing between role classes (sideways moves accepted).  With
+  // threads > 1 the model evaluations of consecutive candidates run
+  // speculatively in parallel and are committed in sequence order, so the
+  // result is the same for every thread count (and on every machine).
   k_free = std::min(k_free, 63);
   std::vector<int8_t> perm(64);
   for (int v = 0; v < 64; v++) perm[v] = (int8_t)v;
   if (k_free <= 5 || base.generic || base.materialised || base.mode != KM_COUNT) return {};
   const int s = base.slot_bits, t = base.thread_bits, m = base.inner_bits;
-  auto role = [&](int q) { return q < 5 ? 0 : q - 5 < s ? 1 : q - 5 < s + t ? 2 : q - 5 < s + t + m ? 3 : 4; };
+  // role classes for the swap moves: lane and thread positions are one class
+  // (both put a cell's cost outside the loops); slot, inner and outer others
+  auto role = [&](int q) { return q < 5 ? 2 : q - 5 < s ? 1 : q - 5 < s + t ? 2 : q - 5 < s + t + m ? 3 : 4; };
   auto eval = [&](const std::vector<int8_t>& pm) {
     KernelSpec spec = base;
     spec.perm = pm;
@@ -939,9 +1022,6 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
   uint64_t rs = seed * 6364136223846793005ull + 1442695040888963407ull;
   auto rnd = [&](uint64_t n) { rs = rs * 6364136223846793005ull + 1442695040888963407ull; return (rs >> 33) % n; };
   threads = std::max(1, std::min(threads, 64));
-  std::vector<int8_t> best = perm;
-  double best_c = eval(best);
-  int evals = 1;
   // evaluate a batch of candidates (in parallel when threads > 1)
   auto eval_batch = [&](const std::vector<std::vector<int8_t>>& cand, std::vector<double>* cost) {
     cost->assign(cand.size(), 0.0);
@@ -958,10 +1038,13 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
       });
     for (auto& x : th) x.join();
   };
-  // random restarts: shuffle the free variables' positions (independent draws)
+  // the identity, the constructive start and random restarts (independent draws)
+  std::vector<int8_t> best = perm;
+  double best_c = 1e300;
+  int evals = 0;
   {
-    const int R = std::min(std::max(1, budget / 4), budget - evals);
-    std::vector<std::vector<int8_t>> cand;
+    std::vector<std::vector<int8_t>> cand{perm, constructive_roles(prog, base, k_free)};
+    const int R = std::max(0, std::min(budget / 16, budget - 2));
     for (int r = 0; r < R; r++) {
       std::vector<int8_t> pm = perm;
       for (int i = k_free - 1; i > 0; i--) std::swap(pm[i], pm[rnd((uint64_t)i + 1)]);
@@ -974,10 +1057,12 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
       if (cost[r] < best_c) { best_c = cost[r]; best = cand[r]; }
     }
   }
-  // hill climbing: swap the positions of two variables with different roles;
-  // candidates are drawn from the current best in sequence, evaluated
-  // speculatively in batches, and the first improvement (in draw order) is
-  // committed -- the generator is rewound to just after it
+  // hill climbing: swap the positions of two variables of different role
+  // classes; candidates are drawn from the current point in sequence,
+  // evaluated speculatively in batches, and the first acceptable one (in
+  // draw order) is committed -- the generator is rewound to just after it
+  std::vector<int8_t> cur = best;
+  double cur_c = best_c;
   int stall = 0;
   while (evals < budget && stall < 100000) {
     std::vector<std::vector<int8_t>> cand;
@@ -985,9 +1070,9 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
     const int B = std::min(threads, budget - evals);
     while ((int)cand.size() < B && stall < 100000) {
       int a = (int)rnd((uint64_t)k_free), c = (int)rnd((uint64_t)k_free);
-      if (role(best[a]) == role(best[c])) { stall++; continue; }
+      if (role(cur[a]) == role(cur[c])) { stall++; continue; }
       stall = 0;
-      std::vector<int8_t> pm = best;
+      std::vector<int8_t> pm = cur;
       std::swap(pm[a], pm[c]);
       cand.push_back(std::move(pm));
       state_after.push_back(rs);
@@ -997,10 +1082,11 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
     eval_batch(cand, &cost);
     for (size_t i = 0; i < cand.size(); i++) {
       evals++;
-      if (cost[i] < best_c) {
-        best_c = cost[i];
-        best = cand[i];
-        rs = state_after[i];   // later candidates were drawn from the old best
+      if (cost[i] <= cur_c) {      // sideways moves too: walks across plateaus
+        cur_c = cost[i];
+        cur = cand[i];
+        if (cur_c < best_c) { best_c = cur_c; best = cur; }
+        rs = state_after[i];       // later candidates were drawn from the old point
         break;
       }
     }
@@ -1181,6 +1267,291 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     st.words_per_iter = (uint32_t)S;
   }
   if (stats) *stats = st;
+  return os.str();
+}
+
+// ============================================================== PTX emission
+// The count-mode specialised kernel (and the work-queue bodies) emitted as
+// PTX directly and compiled by the PTX compiler alone: the same cover, the
+// same schedule and the same loop structure as emit_kernel's CUDA C++ (which
+// NVRTC would first have to translate to this PTX), at half the JIT time.
+namespace {
+
+constexpr const char* kPtxHeader = ".version 8.8\n.target sm_100a\n.address_size 64\n";
+
+std::string ptx_imm(uint32_t w) {
+  char b[16];
+  snprintf(b, sizeof b, "0x%08X", w);
+  return b;
+}
+
+struct PtxEmitter {
+  const Dag& d;
+  std::ostringstream& os;
+  std::map<uint32_t, std::set<std::pair<int, int>>> derived;  // IMAD operand registers per u
+  PtxEmitter(const Dag& dag, std::ostringstream& o) : d(dag), os(o) {}
+
+  std::string reg(uint32_t n) const {
+    const Node& nd = d.nodes[n];
+    if (nd.kind == NK_VAR) return "%v" + std::to_string(nd.val);
+    return "%c" + std::to_string(n);
+  }
+  std::string operand(uint32_t n) const {
+    const Node& nd = d.nodes[n];
+    return nd.kind == NK_CONST ? ptx_imm(nd.val) : reg(n);
+  }
+  static std::string dname(uint32_t u, int k, int c) {
+    auto enc = [](int v) { return v < 0 ? "m" + std::to_string(-v) : std::to_string(v); };
+    return "%d" + std::to_string(u) + "_" + enc(k) + "_" + enc(c);
+  }
+  std::string affine(uint32_t u, int k, int c, bool record) {
+    if (k == 0) return ptx_imm((uint32_t)c);
+    if (k == 1 && c == 0) return reg(u);
+    if (record) derived[u].insert({k, c});
+    return dname(u, k, c);
+  }
+  static void mc(uint8_t f, int* m, int* c) {
+    switch (f) {
+      case 0: *m = 0; *c = 0; break;
+      case 1: *m = 0; *c = -1; break;
+      case 2: *m = 1; *c = 0; break;
+      default: *m = -1; *c = -1; break;
+    }
+  }
+  void plan_cell(const Lut& L) {
+    if (L.kind != 1 || d.nodes[L.in[0]].kind == NK_CONST) return;
+    int m0, c0, m1, c1;
+    mc(L.f0, &m0, &c0);
+    mc(L.f1, &m1, &c1);
+    affine(L.in[1], m0 - m1, m0, true);
+    affine(L.in[1], c0 - c1, c0, true);
+  }
+  void emit_derived(uint32_t u) {
+    auto it = derived.find(u);
+    if (it == derived.end()) return;
+    for (auto& kc : it->second)
+      os << "\tmad.lo.u32 " << dname(u, kc.first, kc.second) << ", " << reg(u) << ", " << ptx_imm((uint32_t)kc.first)
+         << ", " << ptx_imm((uint32_t)kc.second) << ";\n";
+  }
+  void cell(const Lut& L) {
+    if (L.kind == 1) {
+      int m0, c0, m1, c1;
+      mc(L.f0, &m0, &c0);
+      mc(L.f1, &m1, &c1);
+      const Node& xn = d.nodes[L.in[0]];
+      if (xn.kind == NK_CONST) {
+        const uint32_t K = xn.val;
+        const uint32_t K0 = (uint32_t)((int)K * m0 + c0), K1 = (uint32_t)((int)K * m1 + c1);
+        os << "\tmad.lo.u32 " << reg(L.root) << ", " << reg(L.in[1]) << ", " << ptx_imm(K0 - K1) << ", "
+           << ptx_imm(K0) << ";\n";
+      } else {
+        os << "\tmad.lo.u32 " << reg(L.root) << ", " << reg(L.in[0]) << ", " << affine(L.in[1], m0 - m1, m0, false)
+           << ", " << affine(L.in[1], c0 - c1, c0, false) << ";\n";
+      }
+    } else {
+      char imm[8];
+      snprintf(imm, sizeof imm, "0x%02X", L.imm);
+      os << "\tlop3.b32 " << reg(L.root) << ", " << operand(L.in[0]) << ", " << operand(L.in[1]) << ", "
+         << operand(L.in[2]) << ", " << imm << ";\n";
+    }
+    emit_derived(L.root);
+  }
+};
+
+// u64 warp sum of %acc (butterfly), leaves the total in %acc of every lane
+void ptx_warp_sum(std::ostringstream& os) {
+  for (int off = 16; off > 0; off >>= 1)
+    os << "\tmov.b64 {%lo, %hi}, %acc;\n"
+       << "\tshfl.sync.bfly.b32 %lo2, %lo, " << off << ", 31, -1;\n"
+       << "\tshfl.sync.bfly.b32 %hi2, %hi, " << off << ", 31, -1;\n"
+       << "\tmov.b64 %x64, {%lo2, %hi2};\n"
+       << "\tadd.u64 %acc, %acc, %x64;\n";
+}
+
+}  // namespace
+
+std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* stats, uint64_t body_o_count) {
+  KernelStats st;
+  const bool as_body = !spec.body_name.empty();
+  Built b;
+  build_specialised(prog, spec, &b);
+  const Dag& D = b.D;
+  const std::vector<Lit>& outs = b.outs;
+  const int S = b.S, s = b.s, t = b.t, m = b.m;
+  double best_t = 0;
+  MapResult mr = choose_mapping(b, spec, &best_t, &st.imad_cost);
+  dfs_order(&mr, outs);
+  std::vector<uint8_t> used(64, 0);
+  std::vector<uint32_t> var_node(64, 0);
+  for (size_t k = 0; k < D.nodes.size(); k++)
+    if (D.nodes[k].kind == NK_VAR) var_node[D.nodes[k].val] = (uint32_t)k;
+  auto mark = [&](uint32_t n) { if (D.nodes[n].kind == NK_VAR) used[D.nodes[n].val] = 1; };
+  for (const Lut& L : mr.luts) for (int q = 0; q < 3; q++) mark(L.in[q]);
+  for (Lit o : outs) mark(lit_node(o));
+  std::ostringstream body;
+  PtxEmitter E(D, body);
+  for (const Lut& L : mr.luts) E.plan_cell(L);
+  for (auto& kv : E.derived) {
+    const int lv = mr.node_level[kv.first];
+    if (lv == 3) st.derived_inner += (uint32_t)kv.second.size();
+    if (lv == 2) st.derived_outer += (uint32_t)kv.second.size();
+  }
+  auto emit_level = [&](int lvl) {
+    for (const Lut& L : mr.luts) {
+      if (L.level != lvl) continue;
+      E.cell(L);
+      uint32_t* luts = lvl == 1 ? &st.luts_thread : lvl == 2 ? &st.luts_outer : &st.luts_inner;
+      uint32_t* imads = lvl == 1 ? &st.imads_thread : lvl == 2 ? &st.imads_outer : &st.imads_inner;
+      (*(L.kind == 1 ? imads : luts))++;
+    }
+  };
+  auto level_of = [&](int v) { return (int)b.var_level[v]; };
+  const int unit = s + t + m;
+  // ---- prologue: chunk bounds and thread-level variables/cells
+  body << "\tmov.u32 %tidr, %tid.x;\n";
+  if (as_body) {
+    body << "\tld.param.u64 %cnt, [p_count];\n\tld.param.u32 %bid, [p_bid];\n\tld.param.u32 %nb, [p_nb];\n"
+         << "\tmov.u64 %A, 0;\n\tmov.u64 %O, " << body_o_count << ";\n";
+  } else {
+    body << "\tld.param.u64 %A, [p_A];\n\tld.param.u64 %O, [p_O];\n\tld.param.u64 %cnt, [p_count];\n"
+         << "\tmov.u32 %bid, %ctaid.x;\n\tmov.u32 %nb, %nctaid.x;\n";
+  }
+  body << "\tcvta.to.global.u64 %cnt, %cnt;\n"
+       << "\tcvt.u64.u32 %b, %bid;\n\tcvt.u64.u32 %x64, %nb;\n"
+       << "\tdiv.u64 %q, %O, %x64;\n\trem.u64 %rr, %O, %x64;\n"
+       << "\tmul.lo.u64 %ob, %b, %q;\n\tmin.u64 %y64, %b, %rr;\n\tadd.u64 %ob, %ob, %y64;\n"
+       << "\tsetp.lt.u64 %p0, %b, %rr;\n\tselp.u64 %y64, 1, 0, %p0;\n"
+       << "\tadd.u64 %oe, %ob, %q;\n\tadd.u64 %oe, %oe, %y64;\n";
+  for (int v = 0; v < 64; v++)
+    if (used[v] && level_of(v) == 1) {
+      body << "\tbfe.u32 %t0, %tidr, " << (b.pos[v] - 5 - s) << ", 1;\n\tneg.s32 %v" << v << ", %t0;\n";
+      E.emit_derived(var_node[v]);
+      st.thread_vars++;
+    }
+  emit_level(1);
+  body << "\tmov.u64 %acc, 0;\n\tmov.u64 %o, %ob;\n"
+       << "\tsetp.ge.u64 %p0, %o, %oe;\n\t@%p0 bra $L_done;\n"
+       << "$L_outer:\n"
+       << "\tshl.b64 %wo, %o, " << unit << ";\n\tadd.u64 %wo, %wo, %A;\n";
+  for (int v = 0; v < 64; v++)
+    if (used[v] && level_of(v) == 2) {
+      body << "\tshr.u64 %x64, %wo, " << (b.pos[v] - 5) << ";\n\tcvt.u32.u64 %t0, %x64;\n"
+           << "\tand.b32 %t0, %t0, 1;\n\tneg.s32 %v" << v << ", %t0;\n";
+      E.emit_derived(var_node[v]);
+      st.outer_vars++;
+    }
+  emit_level(2);
+  body << "\tmov.u32 %a32, 0;\n\tmov.u32 %ii, 0;\n"
+       << "$L_inner:\n";
+  for (int v = 0; v < 64; v++)
+    if (used[v] && level_of(v) == 3) {
+      const int k = b.pos[v] - 5 - s - t;
+      body << "\tshl.b32 %t0, %ii, " << (31 - k) << ";\n\tshr.s32 %v" << v << ", %t0, 31;\n";
+      E.emit_derived(var_node[v]);
+      st.inner_vars++;
+    }
+  emit_level(3);
+  uint32_t const_pop = 0;
+  for (int sl = 0; sl < S; sl++) {
+    const Lit o = outs[sl];
+    const Node& on = D.nodes[lit_node(o)];
+    if (on.kind == NK_CONST) {
+      const_pop += (uint32_t)__builtin_popcount(lit_neg(o) ? ~on.val : on.val);
+      continue;
+    }
+    if (lit_neg(o)) body << "\tnot.b32 %t1, " << E.reg(lit_node(o)) << ";\n\tpopc.b32 %t2, %t1;\n";
+    else body << "\tpopc.b32 %t2, " << E.reg(lit_node(o)) << ";\n";
+    body << "\tadd.u32 %a32, %a32, %t2;\n";
+  }
+  if (const_pop) body << "\tadd.u32 %a32, %a32, " << const_pop << ";\n";
+  body << "\tadd.u32 %ii, %ii, 1;\n\tsetp.lt.u32 %p1, %ii, " << (1u << m) << ";\n\t@%p1 bra $L_inner;\n"
+       << "\tcvt.u64.u32 %x64, %a32;\n\tadd.u64 %acc, %acc, %x64;\n"
+       << "\tadd.u64 %o, %o, 1;\n\tsetp.lt.u64 %p0, %o, %oe;\n\t@%p0 bra $L_outer;\n"
+       << "$L_done:\n";
+  if (spec.count_shift) body << "\tshl.b64 %acc, %acc, " << spec.count_shift << ";\n";
+  ptx_warp_sum(body);
+  body << "\tand.b32 %t0, %tidr, 31;\n";
+  if (as_body) {
+    body << "\tsetp.eq.u32 %p0, %t0, 0;\n\tsetp.ne.u64 %p1, %acc, 0;\n\tand.pred %p0, %p0, %p1;\n"
+         << "\t@%p0 red.global.add.u64 [%cnt], %acc;\n\tret;\n";
+  } else {
+    const int nw = 1 << (t - 5 > 0 ? t - 5 : 0);
+    body << "\tshr.u32 %t1, %tidr, 5;\n\tmov.u32 %t2, bfa_red;\n\tshl.b32 %t1, %t1, 3;\n\tadd.u32 %t2, %t2, %t1;\n"
+         << "\tsetp.eq.u32 %p0, %t0, 0;\n\t@%p0 st.shared.u64 [%t2], %acc;\n\tbar.sync 0;\n"
+         << "\tsetp.ge.u32 %p0, %tidr, 32;\n\t@%p0 bra $L_end;\n"
+         << "\tmov.u64 %acc, 0;\n\tsetp.lt.u32 %p1, %tidr, " << nw << ";\n"
+         << "\tmov.u32 %t2, bfa_red;\n\tshl.b32 %t1, %tidr, 3;\n\tadd.u32 %t2, %t2, %t1;\n"
+         << "\t@%p1 ld.shared.u64 %acc, [%t2];\n";
+    ptx_warp_sum(body);
+    body << "\tsetp.eq.u32 %p0, %tidr, 0;\n\tsetp.ne.u64 %p1, %acc, 0;\n\tand.pred %p0, %p0, %p1;\n"
+         << "\t@%p0 red.global.add.u64 [%cnt], %acc;\n$L_end:\n\tret;\n";
+  }
+  // ---- declarations + signature
+  std::ostringstream os;
+  os << "// generated by libbfa (PTX): count specialised s=" << s << " t=" << t << " m=" << m
+     << (spec.perm.empty() ? "" : " (permuted roles)") << "\n";
+  const std::string bounds = "\t.maxntid " + std::to_string(1 << t) + ", 1, 1\n" +
+                             (spec.min_blocks > 0 ? "\t.minnctapersm " + std::to_string(spec.min_blocks) + "\n" : "");
+  if (as_body) {
+    os << ".func " << spec.body_name << "(.param .b64 p_count, .param .b32 p_bid, .param .b32 p_nb)\n{\n";
+  } else {
+    os << kPtxHeader << ".shared .align 8 .b64 bfa_red[32];\n"
+       << ".visible .entry bfa_kernel(.param .u64 p_A, .param .u64 p_O, .param .u64 p_B, .param .u64 p_out, "
+          ".param .u64 p_count)\n" << bounds << "{\n";
+  }
+  os << "\t.reg .pred %p<2>;\n\t.reg .b32 %t<3>, %c<" << D.nodes.size() << ">, %v<64>;\n"
+     << "\t.reg .b32 %tidr, %bid, %nb, %ii, %a32, %lo, %hi, %lo2, %hi2;\n"
+     << "\t.reg .b64 %A, %O, %cnt, %b, %q, %rr, %ob, %oe, %o, %wo, %acc, %x64, %y64;\n";
+  for (auto& kv : E.derived)
+    for (auto& kc : kv.second) os << "\t.reg .b32 " << PtxEmitter::dname(kv.first, kc.first, kc.second) << ";\n";
+  os << body.str() << "}\n";
+  st.words_per_iter = (uint32_t)S;
+  if (stats) *stats = st;
+  return os.str();
+}
+
+std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::vector<std::string>& body_name,
+                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks) {
+  std::ostringstream os;
+  const size_t nb = body_name.size();
+  os << "// generated by libbfa (PTX): work-queue kernel of " << nb << " programs\n" << kPtxHeader;
+  uint64_t total = 0;
+  os << ".const .align 4 .u32 bfa_qpre[" << nb + 1 << "] = {";
+  for (size_t i = 0; i < nb; i++) {
+    os << (i ? ", " : "") << total;
+    total += chunks[i];
+  }
+  os << ", " << total << "};\n";
+  for (const std::string& b : body_ptx) os << b;
+  os << ".visible .entry bfa_kernel(.param .u64 p_count, .param .u64 p_ctr)\n"
+     << "\t.maxntid " << (1 << thread_bits) << ", 1, 1\n"
+     << (min_blocks > 0 ? "\t.minnctapersm " + std::to_string(min_blocks) + "\n" : "") << "{\n"
+     << "\t.reg .pred %p<4>;\n\t.reg .b32 %c, %lo, %hi, %mid, %k, %tidr, %s, %qv, %sh;\n"
+     << "\t.reg .b64 %cnt, %ctr, %x, %y;\n"
+     << "\t.shared .align 4 .u32 s_chunk;\n"
+     << "\tld.param.u64 %cnt, [p_count];\n\tld.param.u64 %ctr, [p_ctr];\n\tcvta.to.global.u64 %ctr, %ctr;\n"
+     << "\tmov.u32 %tidr, %tid.x;\n\tmov.u32 %sh, s_chunk;\n"
+     << "$Q_loop:\n"
+     << "\tbar.sync 0;\n\tsetp.eq.u32 %p0, %tidr, 0;\n"
+     << "\t@%p0 atom.global.add.u32 %c, [%ctr], 1;\n\t@%p0 st.shared.u32 [%sh], %c;\n\tbar.sync 0;\n"
+     << "\tld.shared.u32 %c, [%sh];\n\tsetp.lt.u32 %p1, %c, " << total << ";\n\t@%p1 bra $Q_work;\n"
+     << "\tmov.u32 %s, %nctaid.x;\n\tadd.u32 %s, %s, " << (uint32_t)(total - 1) << ";\n"
+     << "\tsetp.eq.u32 %p2, %c, %s;\n\tand.pred %p2, %p2, %p0;\n\t@%p2 st.global.u32 [%ctr], 0;\n\tret;\n"
+     << "$Q_work:\n\tmov.u32 %lo, 0;\n\tmov.u32 %hi, " << (nb - 1) << ";\n"
+     << "$Q_bs:\n\tsetp.ge.u32 %p3, %lo, %hi;\n\t@%p3 bra $Q_found;\n"
+     << "\tadd.u32 %mid, %lo, %hi;\n\tadd.u32 %mid, %mid, 1;\n\tshr.u32 %mid, %mid, 1;\n"
+     << "\tmul.wide.u32 %x, %mid, 4;\n\tmov.u64 %y, bfa_qpre;\n\tadd.u64 %x, %y, %x;\n\tld.const.u32 %qv, [%x];\n"
+     << "\tsetp.le.u32 %p3, %qv, %c;\n\t@%p3 mov.u32 %lo, %mid;\n\t@!%p3 sub.u32 %hi, %mid, 1;\n\tbra.uni $Q_bs;\n"
+     << "$Q_found:\n\tmul.wide.u32 %x, %lo, 4;\n\tmov.u64 %y, bfa_qpre;\n\tadd.u64 %x, %y, %x;\n"
+     << "\tld.const.u32 %qv, [%x];\n\tsub.u32 %k, %c, %qv;\n\tbra.uni $Q_dispatch;\n";
+  for (size_t i = 0; i < nb; i++)
+    os << "$Q_b" << i << ":\n\t{\n\t.param .b64 a0;\n\t.param .b32 a1;\n\t.param .b32 a2;\n"
+       << "\tmov.u32 %s, " << chunks[i] << ";\n"
+       << "\tst.param.b64 [a0], %cnt;\n\tst.param.b32 [a1], %k;\n\tst.param.b32 [a2], %s;\n"
+       << "\tcall.uni " << body_name[i] << ", (a0, a1, a2);\n\t}\n\tbra.uni $Q_loop;\n";
+  os << "$Q_targets: .branchtargets ";
+  for (size_t i = 0; i < nb; i++) os << (i ? ", " : "") << "$Q_b" << i;
+  os << ";\n$Q_dispatch:\n\tbrx.idx.uni %lo, $Q_targets;\n}\n";
   return os.str();
 }
 

@@ -187,6 +187,19 @@ double model_cost(const Parsed& prog, const KernelSpec& spec);
 std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& spec, int k_free, int budget, uint64_t seed,
                                  int threads = 1);
 
+// PTX of the count-mode specialised kernel (entry "bfa_kernel", parameters
+// (A, o_count, out_base_w, out, count) as emit_kernel's), or, with
+// spec.body_name set, of a work-queue body `.func body_name(count, bid, nb)`
+// over body_o_count outer iterations from word 0.  Same cover, schedule and
+// loops as emit_kernel; compiled by the PTX compiler without NVRTC.
+std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* stats, uint64_t body_o_count = 0);
+
+// PTX of a work-queue kernel (as emit_queue) over PTX bodies: body_ptx holds
+// the distinct bodies' .func text, body_name[i] / chunks[i] the body and
+// chunk count of queue entry i.
+std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::vector<std::string>& body_name,
+                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks);
+
 // CUDA C++ source of one kernel variant (entry point "bfa_kernel").
 std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);
 

@@ -14,6 +14,7 @@
 // and tails and small problems run on the generic word-per-thread kernel.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <nvPTXCompiler.h>
 #include <nvrtc.h>
 
 #include <sys/stat.h>
@@ -306,11 +307,52 @@ std::string cubin_cache_key(const std::string& src) {
   return h.hex();
 }
 
+// Generated PTX (count-mode kernels, emit_ptx) goes straight to the PTX
+// compiler -- no C++ front end.
+const char* const kPtxOpts[] = {"--gpu-name=sm_100a", "-O3"};
+constexpr int kPtxOptCount = 2;
+
+bool is_ptx_source(const std::string& src) { return src.compare(0, 28, "// generated by libbfa (PTX)") == 0; }
+
+int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
+  nvPTXCompilerHandle h = nullptr;
+  nvPTXCompileResult r = nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str());
+  if (r != NVPTXCOMPILE_SUCCESS) return set_err(BFA_E_JIT, "nvPTXCompilerCreate: %d", (int)r);
+  r = nvPTXCompilerCompile(h, kPtxOptCount, kPtxOpts);
+  if (r != NVPTXCOMPILE_SUCCESS) {
+    size_t n = 0;
+    nvPTXCompilerGetErrorLogSize(h, &n);
+    std::string log(n, '\0');
+    if (n) nvPTXCompilerGetErrorLog(h, &log[0]);
+    nvPTXCompilerDestroy(&h);
+    if (log.size() > 1500) log = log.substr(0, 1500) + "...";
+    return set_err(BFA_E_JIT, "PTX compiler: %d\n%s", (int)r, log.c_str());
+  }
+  size_t sz = 0;
+  nvPTXCompilerGetCompiledProgramSize(h, &sz);
+  cubin->resize(sz);
+  nvPTXCompilerGetCompiledProgram(h, cubin->data());
+  nvPTXCompilerDestroy(&h);
+  return BFA_OK;
+}
+
+std::string ptx_cache_key(const std::string& src) {
+  unsigned major = 0, minor = 0;
+  nvPTXCompilerGetVersion(&major, &minor);
+  bfa::Sha256 h;
+  h.update("bfa-ptx-v1|");
+  h.update(std::to_string(major) + "." + std::to_string(minor) + "|");
+  for (int i = 0; i < kPtxOptCount; i++) h.update(std::string(kPtxOpts[i]) + "|");
+  h.update(src);
+  return h.hex();
+}
+
 int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin, bool use_cache = true) {
-  if (!use_cache) return nvrtc_compile(src, cubin);
-  const std::string name = "k_" + cubin_cache_key(src) + ".cubin";
+  const bool ptx = is_ptx_source(src);
+  if (!use_cache) return ptx ? ptx_compile(src, cubin) : nvrtc_compile(src, cubin);
+  const std::string name = "k_" + (ptx ? ptx_cache_key(src) : cubin_cache_key(src)) + ".cubin";
   if (cache_read(name, cubin)) return BFA_OK;
-  int rc = nvrtc_compile(src, cubin);
+  int rc = ptx ? ptx_compile(src, cubin) : nvrtc_compile(src, cubin);
   if (rc == BFA_OK) cache_write(name, cubin->data(), cubin->size());
   return rc;
 }
@@ -339,11 +381,12 @@ struct Options {
   int queue_bodies = 0;          // > 0: decomposition leaves run as persistent work-queue kernels of <= this many bodies
   int queue_chunk = 65536;       // work-queue chunk size (modelled thread-instructions)
   int queue_inner = 2;           // inner-loop bits of work-queue bodies (-1: inner_bits)
-  int queue_role_budget = 400;   // role-search evaluations per work-queue body
+  int queue_role_budget = 100;   // role-search evaluations per work-queue body
   int split_merge = 0;           // > 0: merge sibling leaves of <= this many gates back into their parent
   int decompose_min_k = 30;      // split_pieces applies to aligned sub-cubes of >= 2^this valuations
   int split_min_vars = 24;       // pieces with <= this many free variables are not split further
   int jit_cache = 1;             // 0: this program neither reads nor writes the persistent JIT cache
+  int ptx = 1;                   // count-mode specialised kernels / work-queue modules emitted as PTX
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -478,11 +521,18 @@ int aligned_k(uint64_t wA, uint64_t wB) {
   return __builtin_ctzll(len) + 5;
 }
 
+// Count-mode specialised kernels are emitted as PTX (option "ptx", default 1).
+bool use_ptx(const bfa_prog* p, const bfa::KernelSpec& spec) {
+  return p->opt.ptx && spec.mode == bfa::KM_COUNT && !spec.generic && !spec.materialised && !spec.fuse_count &&
+         spec.body_name.empty();
+}
+
 // Compile (once) the variant `spec` of p; if dev >= 0 also load it on dev.
 // NVRTC runs outside the program lock, so candidates compile in parallel.
 int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntry** out, CUfunction* fn) {
   bfa_prog* p = const_cast<bfa_prog*>(cp);
-  const std::string key = spec_key(spec);
+  const bool ptx = use_ptx(p, spec);
+  const std::string key = spec_key(spec) + (ptx ? "P" : "");
   JitEntry* e = nullptr;
   {
     std::lock_guard<std::mutex> lk(p->mu);
@@ -491,7 +541,7 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
   }
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
-    ne->source = bfa::emit_kernel(p->parsed, spec, &ne->stats);
+    ne->source = ptx ? bfa::emit_ptx(p->parsed, spec, &ne->stats) : bfa::emit_kernel(p->parsed, spec, &ne->stats);
     int rc = nvrtc_compile_cached(ne->source, &ne->cubin, p->opt.jit_cache);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
@@ -1016,7 +1066,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx;
   return k.str();
 }
 
@@ -1654,9 +1704,9 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     resolve_roles(src, &spec, b.nv);
     b.name = "bfa_body_" + std::to_string(i);
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
-    b.src = bfa::emit_kernel(src->parsed, spec, &b.st);
-    b.hash = bfa::sha256_hex(b.src);
     b.O = (1ull << (b.nv - 5)) >> (b.s + t + b.m);
+    b.src = o.ptx ? bfa::emit_ptx(src->parsed, spec, &b.st, b.O) : bfa::emit_kernel(src->parsed, spec, &b.st);
+    b.hash = bfa::sha256_hex(b.src);
     const double inner = b.st.luts_inner + b.st.imads_inner + b.st.derived_inner;
     const double outer = b.st.luts_outer + b.st.imads_outer + b.st.derived_outer;
     b.size = inner;
@@ -1736,7 +1786,14 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
       qg.im += words * ((b.st.imads_inner + b.st.derived_inner) / S +
                         (b.st.imads_outer + b.st.derived_outer) / (S * it));
     }
-    srcs.push_back(bfa::emit_queue(bsrc, bname, O, ch, t, o.min_blocks));
+    if (o.ptx) {
+      std::vector<std::string> distinct;
+      for (auto& x : bsrc)
+        if (!x.empty()) distinct.push_back(std::move(x));
+      srcs.push_back(bfa::emit_ptx_queue(distinct, bname, ch, t, o.min_blocks));
+    } else {
+      srcs.push_back(bfa::emit_queue(bsrc, bname, O, ch, t, o.min_blocks));
+    }
     qg.src_key = key + "|g" + std::to_string(Q.groups.size());
     Q.chunks += qg.chunks;
     Q.groups.push_back(std::move(qg));
@@ -2000,7 +2057,8 @@ int bfa_last_error_code(void) { return g_err_code; }
 
 int bfa_cache_key(const char* source, char* out, size_t len) {
   if (!source || !out || len < 65) return set_err(BFA_E_ARG, "NULL argument or buffer < 65 bytes");
-  snprintf(out, len, "%s", cubin_cache_key(source).c_str());
+  const std::string src(source);
+  snprintf(out, len, "%s", (is_ptx_source(src) ? ptx_cache_key(src) : cubin_cache_key(src)).c_str());
   return BFA_OK;
 }
 const char* bfa_version(void) { return "bfa 0.1 (sm_100a; NVRTC static)"; }
@@ -2142,6 +2200,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_inner") { if (v < -1 || v > 8) return bad(); p->opt.queue_inner = (int)v; }
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
+  else if (k == "ptx") { if (v < 0 || v > 1) return bad(); p->opt.ptx = (int)v; }
   else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
   else if (k == "split_min_vars") { if (v < 5 || v > 63) return bad(); p->opt.split_min_vars = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
@@ -2797,7 +2856,7 @@ int64_t bfa_dump(const bfa_prog* p, int what, int n, char* buf, size_t len) {
     bfa::KernelSpec spec;
     int rc = spec_for_what_n(p, what, n, &spec);
     if (rc) return rc;
-    s = bfa::emit_kernel(p->parsed, spec, nullptr);
+    s = use_ptx(p, spec) ? bfa::emit_ptx(p->parsed, spec, nullptr) : bfa::emit_kernel(p->parsed, spec, nullptr);
   }
   if (buf && len) snprintf(buf, len, "%s", s.c_str());
   return (int64_t)s.size();

@@ -22,7 +22,7 @@ its preparation cost.
 EXHAUSTIVE = {"slot_bits": 5, "thread_bits": 8, "inner_bits": 4, "dual_pipe": 1, "imad_cost_pct": 50,
               "min_blocks": 0, "kernel_cofactor_bits": 0, "split_pieces": 0}
 
-DECOMPOSED = dict(EXHAUSTIVE, split_pieces=32768, queue_bodies=512, queue_inner=2, queue_role_budget=400)
+DECOMPOSED = dict(EXHAUSTIVE, split_pieces=32768, queue_bodies=512, queue_inner=2, queue_role_budget=100)
 
 
 def apply(prog, preset: dict, **overrides):

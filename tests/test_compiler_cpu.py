@@ -237,13 +237,17 @@ def test_cache_key_is_sha256():
     """The persistent JIT cache key is SHA-256 over salt, NVRTC version,
     options and source (no 64-bit hash collisions can load a wrong cubin)."""
     import hashlib
-    src = bfa.Program(W.posets(3)).dump(1, 9)
+    src = bfa.Program(W.posets(3)).dump(3, 9)          # generic kernel: CUDA C++ through NVRTC
     key = bfa.cache_key(src)
     assert re.fullmatch(r"[0-9a-f]{64}", key)
     opts = "--gpu-architecture=sm_100a|-lineinfo|--std=c++17|"
     expect = hashlib.sha256(("bfa-cubin-v2|12.9|" + opts + src).encode()).hexdigest()
     assert key == expect
     assert bfa.cache_key(src + " ") != key
+    ptx = bfa.Program(W.posets(3)).dump(1, 9)          # specialised count kernel: generated PTX
+    assert ptx.startswith("// generated by libbfa (PTX)")
+    expect = hashlib.sha256(("bfa-ptx-v1|12.9|--gpu-name=sm_100a|-O3|" + ptx).encode()).hexdigest()
+    assert bfa.cache_key(ptx) == expect
 
 
 def test_last_error_code():
