@@ -269,13 +269,26 @@ int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_pro
 
 /* Model enumeration ("all labeled models"; out.txt rows,
  * PAPER.md:1091-1096): the models mu in [mu_lo, mu_hi) (bounds as for
- * bfa_count_range), ascending, into the device list mu_out (capacity
- * entries).  *count_dev (device) receives the total number of models; if it
- * exceeds capacity the list holds an unspecified subset of them.  Meant for
- * sparse results (each model is appended with one atomic per word).
+ * bfa_count_range), in ASCENDING order, into the device list mu_out (the first
+ * `capacity` of them); *count_dev (device) receives the total number of
+ * models.  The range is evaluated chunk by chunk (<= 2^33 valuations, a
+ * 1 GiB device vector allocated and freed inside the call) by the
+ * register-mode eval kernel, and each chunk's set bits are compacted in mu
+ * order (per-tile popcounts, one scan, ordered rewrite: no atomics, no sort).
  * Synchronous on `stream`. */
 int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* mu_out, uint64_t capacity,
                   uint64_t* count_dev, void* stream);
+
+/* out.txt rows (one row per model, a valuation of the
+ * letters): for each of the `count` models mu' in mu_dev (device) of a program
+ * over n_free letters -- e.g. a bfa_assume result -- the valuation of the
+ * original n_all letters, deposit(mu', free_ids) | fixed_values (killed
+ * letters reinstated; free_ids host array of n_free ids, NULL = identity),
+ * written to rows_dev (device, count * (n_all + 1) bytes) as n_all characters
+ * '0'/'1' -- letter id n_all - 1 (the paper's b_1) first -- and '\n'.  Async on
+ * `stream`. */
+int bfa_rows(const uint64_t* mu_dev, uint64_t count, int n_free, const int* free_ids, int n_all,
+             uint64_t fixed_values, char* rows_dev, void* stream);
 
 /* Batched counting (the counting procedure TBA runs
  * one reduced program per c-partition): many programs in

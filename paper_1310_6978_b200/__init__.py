@@ -14,7 +14,7 @@ import json
 import os
 
 __all__ = ["Program", "Batch", "BfaError", "words_for", "reinstate", "last_launch", "fill_generators", "popcount",
-           "peak_int", "lib_path", "version", "cache_key"]
+           "peak_int", "lib_path", "version", "cache_key", "rows"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "libbfa.so")
@@ -47,6 +47,8 @@ _SIGS = {
                               _c.POINTER(_c.c_int), _c.POINTER(_c.c_int)]),
     "bfa_enumerate": (_c.c_int, [_c.c_void_p, _c.c_int, _c.c_uint64, _c.c_uint64, _c.c_void_p, _c.c_uint64,
                                  _c.c_void_p, _c.c_void_p]),
+    "bfa_rows": (_c.c_int, [_c.c_void_p, _c.c_uint64, _c.c_int, _c.POINTER(_c.c_int), _c.c_int, _c.c_uint64,
+                             _c.c_void_p, _c.c_void_p]),
     "bfa_batch_create": (_c.c_int, [_c.POINTER(_c.c_void_p), _c.c_int, _c.POINTER(_c.c_void_p)]),
     "bfa_batch_count": (_c.c_int, [_c.c_void_p, _c.POINTER(_c.c_int), _c.c_void_p, _c.c_void_p]),
     "bfa_batch_free": (None, [_c.c_void_p]),
@@ -339,6 +341,21 @@ def reinstate(mu_free, free_ids, assignment: dict) -> list:
             full |= ((m >> new) & 1) << old
         out.append(full)
     return out
+
+
+def rows(mu, n_all: int, free_ids=None, assignment: dict | None = None, stream=None) -> bytes:
+    """bfa_rows: out.txt rows (one '0'/'1' character per letter, id n_all-1
+    first, then a newline) of the models `mu` (device int64 tensor) of a
+    program over len(free_ids) letters; killed letters from `assignment`."""
+    import torch
+    count = mu.numel()
+    free_ids = list(range(n_all)) if free_ids is None else list(free_ids)
+    fixed = sum((1 << v) for v, b in (assignment or {}).items() if b)
+    out = torch.empty(max(1, count * (n_all + 1)), dtype=torch.uint8, device=mu.device if count else "cuda")
+    ids = (ctypes.c_int * max(1, len(free_ids)))(*free_ids)
+    _check(_load().bfa_rows(ctypes.c_void_p(mu.data_ptr()) if count else None, count, len(free_ids), ids, n_all,
+                            fixed, ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return bytes(out[:count * (n_all + 1)].cpu().numpy())
 
 
 def _err_code() -> int:

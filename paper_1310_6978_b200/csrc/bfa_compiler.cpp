@@ -752,17 +752,6 @@ const char* kPrelude =
     "typedef unsigned long long u64;\n"
     "struct __align__(16) u32x4 { u32 x, y, z, w; };\n"
     "struct __align__(8) u32x2 { u32 x, y; };\n"
-    "// enumerate mode: append the valuations of the set bits of word w\n"
-    "static __device__ __forceinline__ void bfa_append(u32 r, u64 w, u64* cursor, u64* mu_out, u64 cap) {\n"
-    "  if (!r) return;\n"
-    "  u64 pos = atomicAdd(cursor, (u64)__popc(r));\n"
-    "  while (r) {\n"
-    "    const int j = __ffs(r) - 1;\n"
-    "    r &= r - 1u;\n"
-    "    if (pos < cap) mu_out[pos] = (w << 5) | (u64)j;\n"
-    "    ++pos;\n"
-    "  }\n"
-    "}\n"
     "// per-warp sum, one atomic per warp (device bodies: no block barrier, no static shared memory)\n"
     "static __device__ __forceinline__ void bfa_warp_sum(u64 acc, u64* count) {\n"
     "  #pragma unroll\n"
@@ -1110,8 +1099,6 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   const std::vector<Lit>& outs = b.outs;
   const int S = b.S, s = b.s, t = b.t, m = b.m;
   const bool want_count = spec.mode == KM_COUNT || spec.fuse_count;
-  const bool enumerate = spec.mode == KM_ENUM;
-  const std::string enum_params = enumerate ? ", u64* __restrict__ mu_out, const u64 cap" : "";
   auto level_of = [&](int v) { return (int)b.var_level[v]; };
   auto pos = [&](int v) { return b.pos[v]; };
   double best_t = 0;
@@ -1181,7 +1168,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
   } else if (spec.generic) {
     os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
        << "bfa_kernel(const u64 w_begin, const u64 w_count, const u32 mask, u32* __restrict__ out, u64* __restrict__ count"
-       << enum_params << ") {\n"
+       << ") {\n"
        << "  u64 acc = 0;\n"
        << "  const u64 stride = (u64)gridDim.x * blockDim.x;\n"
        << "  for (u64 k = (u64)blockIdx.x * blockDim.x + threadIdx.x; k < w_count; k += stride) {\n"
@@ -1191,7 +1178,6 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     emit_level(3, "    ");
     os << "    const u32 r = (" << E.value(outs[0]) << ") & mask;\n";
     if (spec.mode == KM_EVAL) os << "    out[k] = r;\n";
-    if (enumerate) os << "    bfa_append(r, w, count, mu_out, cap);\n";
     if (want_count) os << "    acc += __popc(r);\n";
     os << "  }\n";
     if (want_count) os << "  bfa_block_sum(acc, count);\n";
@@ -1203,11 +1189,11 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     if (as_body)
       os << "extern \"C\" __device__ __noinline__ void " << spec.body_name
          << "(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
-         << enum_params << ", const u32 bid_, const u32 nb_) {\n";
+         << ", const u32 bid_, const u32 nb_) {\n";
     else
       os << "extern \"C\" __global__ void __launch_bounds__(" << bounds << ")\n"
          << "bfa_kernel(const u64 A, const u64 o_count, const u64 out_base_w, u32* __restrict__ out, u64* __restrict__ count"
-         << enum_params << ") {\n";
+         << ") {\n";
     os << "  const u32 tid = threadIdx.x;\n"
        << (as_body ? "  const u64 q = o_count / nb_, rr = o_count % nb_, b = bid_;\n"
                    : "  const u64 q = o_count / gridDim.x, rr = o_count % gridDim.x, b = blockIdx.x;\n")
@@ -1247,10 +1233,6 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
         for (int g = 0; g < S; g += 4)
           os << "      *reinterpret_cast<u32x4*>(out + idx + " << g << ") = u32x4{r" << g << ", r" << g + 1
              << ", r" << g + 2 << ", r" << g + 3 << "};\n";
-    }
-    if (enumerate) {
-      os << "      const u64 wbase = wo + ((u64)i << " << (s + t) << ") + ((u64)tid << " << s << ");\n";
-      for (int sl = 0; sl < S; sl++) os << "      bfa_append(r" << sl << ", wbase + " << sl << ", count, mu_out, cap);\n";
     }
     if (want_count) {
       os << "      acc32 += ";

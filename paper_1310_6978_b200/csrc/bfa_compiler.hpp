@@ -120,7 +120,7 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
                    double imad_cost = 0.0);
 
 // ---------------------------------------------------------------- kernels
-enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1, KM_ENUM = 2 };
+enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1 };
 
 struct KernelSpec {
   KernelMode mode = KM_COUNT;

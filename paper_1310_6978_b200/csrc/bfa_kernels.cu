@@ -7,7 +7,6 @@
 //   peak_lop3  : LOP3 issue-rate microbenchmark (the int-ALU denominator)
 // The register-mode kernels are generated per program and JIT-compiled
 // (bfa_compiler.cpp / bfa_runtime.cpp).
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -296,24 +295,189 @@ cudaError_t interp(const uint32_t* ops, int n_ops, const uint32_t* consts, int n
   return e;
 }
 
-cudaError_t sort_u64(uint64_t* keys, uint64_t n, int end_bit, cudaStream_t st) {
-  size_t temp = 0;
-  unsigned long long* k = reinterpret_cast<unsigned long long*>(keys);
-  cudaError_t e = cub::DeviceRadixSort::SortKeys(nullptr, temp, k, k, (int64_t)n, 0, end_bit, st);
+}  // namespace bfa_k
+
+namespace {
+
+// ---------------------------------------------------------------- ordered compaction
+// Models of a materialised DNF vector in ascending mu (
+// PAPER.md:576-580 "all labeled models"): a tile of kTileWords u64 words per
+// block, (1) per-tile popcounts, (2) one exclusive scan over the tiles (plus
+// the running total of earlier chunks), (3) every tile rewrites its set bits
+// at its offset: thread prefix by warp shuffles and a block scan, so the
+// output order is the mu order with no atomics and no sort.
+constexpr int kCompactThreads = 256, kWordsPerThread = 4;
+constexpr int kTileWords = kCompactThreads * kWordsPerThread;
+
+// bit j of word w is valuation base + 64 w + j; only [lo, hi) (relative to
+// base) count
+__device__ __forceinline__ u64 masked_word(const u64* v, u64 w, u64 n_words, u64 lo, u64 hi) {
+  if (w >= n_words) return 0ull;
+  u64 x = v[w];
+  const u64 b0 = w * 64;
+  if (b0 < lo) x &= (lo - b0 >= 64) ? 0ull : (~0ull << (lo - b0));
+  if (b0 + 64 > hi) x &= (hi <= b0) ? 0ull : (hi - b0 >= 64 ? ~0ull : ((1ull << (hi - b0)) - 1ull));
+  return x;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) tile_popc_kernel(const u64* __restrict__ v, u64 n_words, u64 lo,
+                                                                   u64 hi, u32* __restrict__ tile_count) {
+  const u64 w0 = (u64)blockIdx.x * kTileWords + (u64)threadIdx.x * kWordsPerThread;
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < kWordsPerThread; j++) c += __popcll(masked_word(v, w0 + j, n_words, lo, hi));
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ u32 red[kCompactThreads / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    u32 t = threadIdx.x < kCompactThreads / 32 ? red[threadIdx.x] : 0u;
+    t = __reduce_add_sync(0xffffffffu, t);
+    if (threadIdx.x == 0) tile_count[blockIdx.x] = t;
+  }
+}
+
+// one block: exclusive scan of n tile counts into u64 offsets starting at
+// *running; *running += the total
+__global__ void __launch_bounds__(1024) tile_scan_kernel(const u32* __restrict__ cnt, u64 n, u64* __restrict__ off,
+                                                         u64* __restrict__ running) {
+  __shared__ u64 warp_tot[32];
+  __shared__ u64 carry;
+  const u32 tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) carry = *running;
+  __syncthreads();
+  for (u64 b0 = 0; b0 < n; b0 += 1024) {
+    const u64 i = b0 + tid;
+    const u64 x = i < n ? (u64)cnt[i] : 0ull;
+    u64 inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u64 y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= (u32)d) inc += y;
+    }
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      u64 t = warp_tot[lane], ti = t;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const u64 y = __shfl_up_sync(0xffffffffu, ti, d);
+        if (lane >= (u32)d) ti += y;
+      }
+      warp_tot[lane] = ti - t;  // exclusive prefix of the warp totals
+    }
+    __syncthreads();
+    const u64 c0 = carry;
+    if (i < n) off[i] = c0 + warp_tot[wid] + inc - x;
+    __syncthreads();
+    if (tid == 1023) carry = c0 + warp_tot[wid] + inc;
+    __syncthreads();
+  }
+  if (tid == 0) *running = carry;
+}
+
+__global__ void __launch_bounds__(kCompactThreads) tile_write_kernel(const u64* __restrict__ v, u64 n_words, u64 lo,
+                                                                    u64 hi, u64 base, const u64* __restrict__ off,
+                                                                    u64* __restrict__ mu_out, u64 cap) {
+  const u32 tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const u64 w0 = (u64)blockIdx.x * kTileWords + (u64)tid * kWordsPerThread;
+  u64 x[kWordsPerThread];
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < kWordsPerThread; j++) {
+    x[j] = masked_word(v, w0 + j, n_words, lo, hi);
+    c += __popcll(x[j]);
+  }
+  // exclusive prefix of c over the block (warp shuffles + one smem pass)
+  u32 inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u32 y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= (u32)d) inc += y;
+  }
+  __shared__ u32 wsum[kCompactThreads / 32];
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  u32 before = 0;
+  for (u32 k = 0; k < wid; k++) before += wsum[k];
+  u64 pos = off[blockIdx.x] + before + inc - c;
+#pragma unroll
+  for (int j = 0; j < kWordsPerThread; j++) {
+    u64 r = x[j];
+    const u64 mu0 = base + (w0 + j) * 64;
+    while (r) {
+      const int b = __ffsll((long long)r) - 1;
+      r &= r - 1;
+      if (pos < cap) mu_out[pos] = mu0 + (u64)b;
+      ++pos;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- out.txt rows
+// One row per model: the model mu' of the (possibly
+// assumed) program is deposited on the original letter ids (killed letters
+// reinstated from fixed_values), then written as n_all characters '0'/'1',
+// the paper's b_1 (id n_all - 1) first, and '\n'.
+__constant__ int c_free_ids[64];
+
+__global__ void __launch_bounds__(256) rows_kernel(const u64* __restrict__ mu, u64 count, int n_free, int n_all,
+                                                   u64 fixed_values, char* __restrict__ rows) {
+  const u64 stride = (u64)gridDim.x * blockDim.x;
+  for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += stride) {
+    const u64 m = mu[r];
+    u64 full = fixed_values;
+    for (int k = 0; k < n_free; k++) full |= ((m >> k) & 1ull) << c_free_ids[k];
+    char* row = rows + r * (u64)(n_all + 1);
+    for (int j = 0; j < n_all; j++) row[j] = (char)('0' + ((full >> (n_all - 1 - j)) & 1ull));
+    row[n_all] = '\n';
+  }
+}
+
+}  // namespace
+
+namespace bfa_k {
+
+cudaError_t compact_models(const uint64_t* vec, uint64_t n_words, uint64_t lo, uint64_t hi, uint64_t base,
+                           uint64_t* mu_out, uint64_t cap, uint64_t* running, cudaStream_t st) {
+  const u64 tiles = (n_words + kTileWords - 1) / kTileWords;
+  if (!tiles) return cudaSuccess;
+  if (tiles > 0x7fffffffull) return cudaErrorInvalidValue;
+  u32* cnt = nullptr;
+  u64* off = nullptr;
+  cudaError_t e = cudaMallocAsync(&cnt, tiles * 4, st);
   if (e != cudaSuccess) return e;
-  unsigned long long* alt = nullptr;
-  void* tmp = nullptr;
-  if ((e = cudaMallocAsync(&alt, n * 8, st)) != cudaSuccess) return e;
-  if ((e = cudaMallocAsync(&tmp, temp, st)) != cudaSuccess) { cudaFreeAsync(alt, st); return e; }
-  cub::DoubleBuffer<unsigned long long> db(k, alt);
-  e = cub::DeviceRadixSort::SortKeys(tmp, temp, db, (int64_t)n, 0, end_bit, st);
-  if (e == cudaSuccess && db.Current() != k) e = cudaMemcpyAsync(k, db.Current(), n * 8, cudaMemcpyDeviceToDevice, st);
-  cudaFreeAsync(tmp, st);
-  cudaFreeAsync(alt, st);
+  if ((e = cudaMallocAsync(&off, tiles * 8, st)) != cudaSuccess) { cudaFreeAsync(cnt, st); return e; }
+  const u64* v = reinterpret_cast<const u64*>(vec);
+  tile_popc_kernel<<<(unsigned)tiles, kCompactThreads, 0, st>>>(v, n_words, lo, hi, cnt);
+  tile_scan_kernel<<<1, 1024, 0, st>>>(cnt, tiles, off, reinterpret_cast<u64*>(running));
+  tile_write_kernel<<<(unsigned)tiles, kCompactThreads, 0, st>>>(v, n_words, lo, hi, base, off,
+                                                                 reinterpret_cast<u64*>(mu_out), cap);
+  e = cudaGetLastError();
+  cudaFreeAsync(off, st);
+  cudaFreeAsync(cnt, st);
   return e;
 }
 
+cudaError_t rows(const uint64_t* mu, uint64_t count, int n_free, const int* free_ids, int n_all,
+                 uint64_t fixed_values, char* out, cudaStream_t st) {
+  cudaError_t e = cudaMemcpyToSymbolAsync(c_free_ids, free_ids, sizeof(int) * n_free, 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  if (!count) return cudaSuccess;
+  const unsigned grid = (unsigned)std::min<u64>((count + 255) / 256, 148ull * 8);
+  rows_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const u64*>(mu), count, n_free, n_all, fixed_values, out);
+  return cudaGetLastError();
+}
+
+}  // namespace bfa_k
+
+namespace {
+
 __global__ void add_u64_kernel(u64* dst, const u64* src) { *dst += *src; }
+
+}  // namespace
+
+namespace bfa_k {
 
 cudaError_t add_u64(uint64_t* dst, const uint64_t* src, cudaStream_t st) {
   add_u64_kernel<<<1, 1, 0, st>>>(reinterpret_cast<u64*>(dst), reinterpret_cast<const u64*>(src));

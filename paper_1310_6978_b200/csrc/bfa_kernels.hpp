@@ -15,8 +15,16 @@ cudaError_t popcount(const uint64_t* v, uint64_t n_words, uint64_t* count, cudaS
 cudaError_t interp(const uint32_t* ops, int n_ops, const uint32_t* consts, int n_consts, int n_slots,
                    uint32_t out_op, int out_neg, uint64_t w_begin, uint64_t w_count, uint32_t mask, uint32_t* out,
                    uint64_t* count, cudaStream_t st, int* block_used);
-// ascending radix sort of n u64 keys in place (bits [0, end_bit))
-cudaError_t sort_u64(uint64_t* keys, uint64_t n, int end_bit, cudaStream_t st);
+// ordered compaction: append the set bits of vec[0..n_words) whose index
+// (relative to the vector) lies in [lo, hi) as valuations base + index, in
+// ascending order, at positions *running.. of mu_out (< cap written);
+// *running (device) += their number.  No atomics, no sort.
+cudaError_t compact_models(const uint64_t* vec, uint64_t n_words, uint64_t lo, uint64_t hi, uint64_t base,
+                           uint64_t* mu_out, uint64_t cap, uint64_t* running, cudaStream_t st);
+// out.txt rows: row r = the letters of deposit(mu[r], free_ids) | fixed_values,
+// id n_all-1 first, as '0'/'1', then '\n' (n_all + 1 bytes per row)
+cudaError_t rows(const uint64_t* mu, uint64_t count, int n_free, const int* free_ids, int n_all,
+                 uint64_t fixed_values, char* out, cudaStream_t st);
 // *dst += *src on the device
 cudaError_t add_u64(uint64_t* dst, const uint64_t* src, cudaStream_t st);
 // op 0: lop3.b32, 1: mad.lo.u32, 2: both 1:1 -- 256 ops per thread per iteration

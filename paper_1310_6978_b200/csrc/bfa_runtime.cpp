@@ -653,8 +653,7 @@ std::vector<Segment> plan(const Options& o, int s, int n, uint64_t wlo, uint64_t
 
 // Common body of count_range / eval_range.
 int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-                   cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out, uint64_t cap, bool accumulate) {
-  const bool enumerate = mu_out != nullptr;
+                   cudaStream_t st, bool eval, int force_roles_k, bool accumulate) {
   if (!p) return set_err(BFA_E_ARG, "NULL program");
   if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
   if (p->info.max_var_id >= n)
@@ -669,7 +668,6 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
                    (unsigned long long)align);
   if (eval && !out_dev) return set_err(BFA_E_ARG, "NULL output buffer");
   if (!eval && !count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
-  if (enumerate && (eval || p->opt.engine == 1)) return set_err(BFA_E_ARG, "enumerate: JIT count path only");
   int dev;
   DevInfo di;
   int rc = current_device(&dev, &di);
@@ -719,7 +717,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
   }
   const int T = 1 << o.thread_bits;
   const int seg = o.segment_cells ? o.segment_cells : (p->info.luts > 8000 ? 768 : 0);
-  if (seg > 0 && !enumerate) {
+  if (seg > 0) {
     // NEXT-3: program too large for one straight-line kernel -> segments
     bfa_prog* mp = const_cast<bfa_prog*>(p);
     const bfa::KernelMode mode = eval ? bfa::KM_EVAL : bfa::KM_COUNT;
@@ -816,7 +814,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
   for (size_t k = 0; k < segs.size(); k++) {
     const Segment& sg = segs[k];
     bfa::KernelSpec spec;
-    spec.mode = eval ? bfa::KM_EVAL : enumerate ? bfa::KM_ENUM : bfa::KM_COUNT;
+    spec.mode = eval ? bfa::KM_EVAL : bfa::KM_COUNT;
     spec.generic = sg.generic;
     spec.slot_bits = sg.generic ? 0 : s_eff;
     spec.thread_bits = o.thread_bits;
@@ -840,14 +838,14 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
       uint64_t wb = sg.wb, wc = sg.we - sg.wb;
       uint32_t* o32 = eval ? out32 + (sg.wb - wlo) : nullptr;
       grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((wc + T - 1) / T, grid_cap));
-      void* args[] = {&wb, &wc, &mask, &o32, &cnt, &mu_out, &cap};
+      void* args[] = {&wb, &wc, &mask, &o32, &cnt};
       rc = launch(fn, grid, T, st, args);
     } else {
       const int ub = s_eff + o.thread_bits + sg.m;
       uint64_t A = sg.wb, O = (sg.we - sg.wb) >> ub, base = wlo;
       uint32_t* o32 = out32;
       grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(O, grid_cap));
-      void* args[] = {&A, &O, &base, &o32, &cnt, &mu_out, &cap};
+      void* args[] = {&A, &O, &base, &o32, &cnt};
       rc = launch(fn, grid, T, st, args);
     }
     if (rc) return rc;
@@ -924,11 +922,9 @@ int count_positions(const bfa_prog* p, int n, int k_free, uint64_t pos_lo, uint6
   uint64_t A = pos_lo >> 5, O = (pos_hi - pos_lo) >> (ub + 5), base = 0;
   uint32_t* o32 = nullptr;
   uint64_t* cnt = count_dev;
-  uint64_t* mu_out = nullptr;
-  uint64_t cap = 0;
   const int bps = p->opt.blocks_per_sm ? p->opt.blocks_per_sm : je->occupancy[dev];
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(O, (uint64_t)di.sms * bps));
-  void* args[] = {&A, &O, &base, &o32, &cnt, &mu_out, &cap};
+  void* args[] = {&A, &O, &base, &o32, &cnt};
   return launch(fn, grid, 1 << spec.thread_bits, st, args);
 }
 
@@ -992,10 +988,9 @@ int prepare_count(const bfa_prog* p, int n, int sms) {
 int decompose_count(const bfa_prog* p, int n, uint64_t mu_lo, int k, uint64_t* count_dev, cudaStream_t st);
 
 int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
-                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out,
-                     uint64_t cap);
+                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k);
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval, int force_roles_k = -1, uint64_t* mu_out = nullptr, uint64_t cap = 0);
+              cudaStream_t st, bool eval, int force_roles_k = -1);
 
 // Multi-launch counts replay as a CUDA graph: the first call of a key runs
 // directly (and prepares every kernel), the second captures the launch
@@ -1071,18 +1066,18 @@ std::string options_key(const Options& o) {
 }
 
 int run_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev, uint64_t* count_dev,
-              cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out, uint64_t cap) {
+              cudaStream_t st, bool eval, int force_roles_k) {
   if (p && !g_forked) g_fork_width = p->opt.streams;
   const bool multi = p && (p->opt.split_pieces > 1 || p->opt.kernel_cofactor_bits > 0);
-  if (!multi || !p->opt.graphs || eval || mu_out || force_roles_k >= 0 || !count_dev)
-    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap);
+  if (!multi || !p->opt.graphs || eval || force_roles_k >= 0 || !count_dev)
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k);
   int dev = 0;
   cudaGetDevice(&dev);
   std::ostringstream k;
   k << "range|" << dev << '.' << n << '.' << mu_lo << '.' << mu_hi << '.' << (uintptr_t)count_dev << '.'
     << (uintptr_t)g_caller_stream << '|' << options_key(p->opt);
   return with_graph(p, k.str(), st, [&](cudaStream_t s) {
-    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, s, eval, force_roles_k, mu_out, cap);
+    return run_range_direct(p, n, mu_lo, mu_hi, out_dev, count_dev, s, eval, force_roles_k);
   });
 }
 
@@ -1228,21 +1223,20 @@ int multi_body_count(bfa_prog* mp, const std::string& kkey, std::vector<std::uni
 }
 
 int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* out_dev,
-                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k, uint64_t* mu_out,
-                     uint64_t cap) {
-  if (p && !eval && !mu_out && force_roles_k < 0 && p->opt.split_pieces > 1 && n <= 63 && p->info.max_var_id < n &&
+                     uint64_t* count_dev, cudaStream_t st, bool eval, int force_roles_k) {
+  if (p && !eval && force_roles_k < 0 && p->opt.split_pieces > 1 && n <= 63 && p->info.max_var_id < n &&
       mu_hi <= (1ull << n) && mu_lo < mu_hi && !(mu_lo & 31) && !(mu_hi & 31) && count_dev &&
       p->info.luts <= 8000 && !p->opt.segment_cells) {
     const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
     if (k >= p->opt.decompose_min_k) return decompose_count(p, n, mu_lo, k, count_dev, st);
   }
   const int j = p ? p->opt.kernel_cofactor_bits : 0;
-  if (!p || eval || mu_out || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
+  if (!p || eval || j == 0 || force_roles_k >= 0 || n > 63 || p->info.max_var_id >= n ||
       mu_hi > (1ull << n) || mu_lo >= mu_hi)
-    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, g_accumulate);
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, g_accumulate);
   const int k = aligned_k(mu_lo >> 5, mu_hi >> 5);
   if ((mu_lo & 31) || (mu_hi & 31) || k < 24 + j || p->info.luts > 8000 || p->opt.segment_cells)
-    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, mu_out, cap, g_accumulate);
+    return run_range_core(p, n, mu_lo, mu_hi, out_dev, count_dev, st, eval, force_roles_k, g_accumulate);
   if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
   int dev;
   DevInfo di;
@@ -1284,7 +1278,7 @@ int run_range_direct(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, u
     if (q->info.const_value == 0) { zero++; continue; }
     if (q->info.const_value == 1) one++;
     g_cells_lop3 = g_cells_imad = 0;
-    rc = run_range_core(q.get(), kk, 0, 1ull << kk, nullptr, count_dev, fork.stream(), false, -1, nullptr, 0, true);
+    rc = run_range_core(q.get(), kk, 0, 1ull << kk, nullptr, count_dev, fork.stream(), false, -1, true);
     if (rc) return rc;
     l3 += g_cells_lop3;
     im += g_cells_imad;
@@ -1893,7 +1887,7 @@ int count_pieces(std::vector<std::unique_ptr<bfa_prog>>& kids, const std::vector
       rc = run_range(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, ps, false);
       g_accumulate = false;
     } else {
-      rc = run_range_core(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, ps, false, -1, nullptr, 0, true);
+      rc = run_range_core(kids[i].get(), nv, 0, 1ull << nv, nullptr, count_dev, ps, false, -1, true);
     }
     if (rc) return rc;
     l3 += g_cells_lop3;
@@ -2128,33 +2122,67 @@ int bfa_assume(const bfa_prog* p, int n, uint64_t mask, uint64_t values, bfa_pro
 
 int bfa_enumerate(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uint64_t* mu_out, uint64_t capacity,
                   uint64_t* count_dev, void* stream) {
+  // The models are the set bits of the DNF vector (Prop 2.2): evaluate the
+  // range chunk by chunk into a device vector with the register-mode eval
+  // kernel, then compact each chunk's set bits in mu order (tile popcounts,
+  // one scan, ordered rewrite; bfa_kernels.cu) -- ascending by construction.
+  if (!p) return set_err(BFA_E_ARG, "NULL program");
   if (!mu_out && capacity) return set_err(BFA_E_ARG, "NULL output list");
   if (!count_dev) return set_err(BFA_E_ARG, "NULL count pointer");
+  if (n < 0 || n > 63) return set_err(BFA_E_RANGE, "n=%d outside [0, 63]", n);
+  if (p->info.max_var_id >= n)
+    return set_err(BFA_E_RANGE, "program uses x%d, needs n > %d (got n=%d)", p->info.max_var_id, p->info.max_var_id, n);
+  const uint64_t full = 1ull << n;
+  if (mu_lo > mu_hi || mu_hi > full) return set_err(BFA_E_RANGE, "valuation range outside [0, 2^n)");
+  if (!(mu_lo == 0 && mu_hi == full) && ((mu_lo % 32) || (mu_hi % 32)))
+    return set_err(BFA_E_ARG, "range bounds must be multiples of 32 (or the whole range)");
   cudaStream_t st = (cudaStream_t)stream;
   g_caller_stream = st;
-  uint64_t dummy_cap = capacity;
-  uint64_t* list = mu_out;
-  uint64_t* scratch = nullptr;
-  if (!list) {  // count-only call still needs a valid pointer
-    if (cudaMallocAsync(&scratch, 8, st) != cudaSuccess) return set_err(BFA_E_NOMEM, "cudaMallocAsync");
-    list = scratch;
-    dummy_cap = 0;
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaError_t e = cudaMemsetAsync(count_dev, 0, sizeof(uint64_t), st);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e));
+  if (mu_hi == mu_lo) return cudaStreamSynchronize(st) == cudaSuccess ? BFA_OK : set_err(BFA_E_CUDA, "sync");
+  // 64-aligned evaluation range covering [mu_lo, mu_hi), in chunks of <= 2^33
+  // valuations (a 1 GiB vector)
+  const uint64_t elo = n < 6 ? 0 : mu_lo & ~63ull;
+  const uint64_t ehi = n < 6 ? full : std::min<uint64_t>(full, (mu_hi + 63) & ~63ull);
+  const uint64_t chunk = std::min<uint64_t>(ehi - elo, 1ull << 33);
+  uint64_t* vec = nullptr;
+  const uint64_t vwords = std::max<uint64_t>(1, (chunk + 63) / 64);
+  if (cudaMallocAsync(&vec, vwords * 8, st) != cudaSuccess)
+    return set_err(BFA_E_NOMEM, "enumerate: %llu-word vector", (unsigned long long)vwords);
+  for (uint64_t c0 = elo; c0 < ehi && rc == BFA_OK; c0 += chunk) {
+    const uint64_t c1 = std::min(ehi, c0 + chunk);
+    rc = run_range(p, n, c0, c1, vec, nullptr, st, true);
+    if (rc) break;
+    const uint64_t lo = std::max(mu_lo, c0) - c0, hi = std::min(mu_hi, c1) - c0;
+    e = bfa_k::compact_models(vec, (c1 - c0 + 63) / 64, lo, hi, c0, mu_out, mu_out ? capacity : 0, count_dev, st);
+    if (e != cudaSuccess) rc = set_err(BFA_E_CUDA, "enumerate compaction: %s", cudaGetErrorString(e));
   }
-  int rc = run_range(p, n, mu_lo, mu_hi, nullptr, count_dev, st, false, -1, list, dummy_cap);
-  if (rc) { if (scratch) cudaFreeAsync(scratch, st); return rc; }
-  uint64_t found = 0;
-  cudaError_t e = cudaMemcpyAsync(&found, count_dev, 8, cudaMemcpyDeviceToHost, st);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-  if (scratch) cudaFreeAsync(scratch, st);
+  cudaFreeAsync(vec, st);
+  e = cudaStreamSynchronize(st);
+  if (rc) return rc;
   if (e != cudaSuccess) return set_err(BFA_E_CUDA, "enumerate: %s", cudaGetErrorString(e));
-  const uint64_t m = std::min(found, capacity);
-  if (m > 1) {
-    int bits = 1;
-    while (bits < 64 && (mu_hi - 1) >> bits) bits++;
-    e = bfa_k::sort_u64(list, m, bits, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) return set_err(BFA_E_CUDA, "enumerate sort: %s", cudaGetErrorString(e));
+  return BFA_OK;
+}
+
+int bfa_rows(const uint64_t* mu_dev, uint64_t count, int n_free, const int* free_ids, int n_all,
+             uint64_t fixed_values, char* rows_dev, void* stream) {
+  if ((!mu_dev || !rows_dev) && count) return set_err(BFA_E_ARG, "NULL argument");
+  if (n_all < 1 || n_all > 64 || n_free < 0 || n_free > n_all) return set_err(BFA_E_RANGE, "bad letter counts");
+  std::vector<int> ids(64, 0);
+  for (int k = 0; k < n_free; k++) {
+    const int id = free_ids ? free_ids[k] : k;
+    if (id < 0 || id >= n_all) return set_err(BFA_E_ARG, "free id %d outside [0, %d)", id, n_all);
+    ids[k] = id;
   }
+  int dev;
+  int rc = current_device(&dev, nullptr);
+  if (rc) return rc;
+  cudaError_t e = bfa_k::rows(mu_dev, count, n_free, ids.data(), n_all, fixed_values, rows_dev, (cudaStream_t)stream);
+  if (e != cudaSuccess) return set_err(BFA_E_CUDA, "rows: %s", cudaGetErrorString(e));
   return BFA_OK;
 }
 

@@ -603,6 +603,33 @@ def test_special_posets_assumptions():
             assert c == oracle.count(red, nf)
 
 
+def test_rows_out_txt(golden):
+    """out.txt rows: one row per model, one character per
+    letter with id n-1 (the paper's b_1) first, so a row read as a binary
+    number is its valuation mu.  C1 rows equal the golden model list; for
+    bounded posets on 7 points the rows of the killed program (34 letters
+    fixed) carry the killed letters reinstated and each
+    row satisfies the unreduced theory (oracle)."""
+    g = golden("c1_posets3.json")
+    mus, total = bfa.Program(W.posets(3)).enumerate(9)
+    lines = bfa.rows(mus, 9).decode().split("\n")
+    assert lines[-1] == "" and all(len(x) == 9 for x in lines[:-1])
+    assert [int(x, 2) for x in lines[:-1]] == g["set_bits"]
+    k = 7
+    text = W.posets(k)
+    a = W.bounded_poset_kills(k)
+    q, nf, ids = bfa.Program(text).assume(k * k, a)
+    mus, total = q.enumerate(nf, capacity=1 << 16)
+    assert total == 4231
+    lines = bfa.rows(mus, k * k, ids, a).decode().splitlines()
+    assert len(lines) == 4231
+    want = bfa.reinstate(mus.cpu().numpy(), ids, a)
+    assert [int(x, 2) for x in lines] == want
+    for x in lines[::211]:
+        mu = int(x, 2)
+        assert oracle.count(text, k * k, mu, mu + 1) == 1
+
+
 def test_enumerate_matches_oracle(golden):
     g = golden("c1_posets3.json")
     mus, total = bfa.Program(W.posets(3)).enumerate(9)
@@ -625,8 +652,14 @@ def test_enumerate_matches_oracle(golden):
     ow, oc = oracle.evaluate(text, n, lo, lo + (1 << 24))
     mus, total = bfa.Program(text).enumerate(n, lo, lo + (1 << 24), capacity=1 << 16)
     assert total == oc and np.array_equal(mus.cpu().numpy(), oracle.set_bits(ow, lo))
-    _, total = bfa.Program(text).enumerate(n, capacity=4)
+    first, total = bfa.Program(text).enumerate(n, capacity=4)
     assert total == 130023
+    ow, _ = oracle.evaluate(text, n, (1 << 36) - (1 << 30), 1 << 36)   # the models are in mu order:
+    top = oracle.set_bits(ow, (1 << 36) - (1 << 30))                 # the first four are the smallest
+    allm, _ = bfa.Program(text).enumerate(n, capacity=1 << 18)
+    assert len(allm) == 130023 and (np.diff(allm.cpu().numpy()) > 0).all()
+    assert first.cpu().tolist() == allm[:4].cpu().tolist()
+    assert np.array_equal(allm.cpu().numpy()[-len(top):], top)
 
 
 # ------------------------------------------------------------ materialised mode
