@@ -136,6 +136,11 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
  *                   leaves of <= this many gates each back into their parent
  *                   (default 0)
+ *   "tune_counts"   bfa_autotune's objective: preparation + tune_counts x the
+ *                   time of one count (default 1)
+ *   "ptx"           1: count-mode specialised kernels and work-queue modules
+ *                   are emitted as PTX for the PTX compiler (default); 0: as
+ *                   CUDA C++ through NVRTC
  *   "jit_cache"     0: this program neither reads nor writes the persistent JIT
  *                   cache (cubins, role searches); every compile is cold
  *                   (default 1)
@@ -149,15 +154,22 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  * Returns BFA_E_ARG for an unknown key or an out-of-range value. */
 int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
 
-/* Empirical autotuning of the register-mode kernel for n variables: JIT
- * compiles a set of candidate variants (slot bits, inner-loop bits, IMAD/LOP3
- * balance) in parallel, times each on the top min(2^n, 2^36) valuations with
- * CUDA events on `stream` -- each candidate with the variable roles (count
- * mode) searched for the whole 2^n cube, as a full count would use -- and sets
- * p's options to the fastest.  Writes a JSON
- * report (candidates, times, choice) to report (nullable).  Results do not
- * depend on the options; only speed does.  Not thread-safe with other calls on
- * the same program.  n < 24: no-op. */
+/* Plan selection for counting over 2^n valuations by the caller's TOTAL
+ * cost: preparation (role searches, decomposition, JIT) + tune_counts x the
+ * time of one count (option "tune_counts", default 1 = a single cold count).
+ * Tries, in order, (A) the current options as one exhaustive kernel, (B) the
+ * kernel-variant sweep (slot bits, inner-loop bits, IMAD/LOP3 balance,
+ * register caps: ~18 variants JIT-compiled in parallel and timed on a probe of
+ * <= 2^36 valuations; only when 30 % of tune_counts x A's count time exceeds
+ * its predicted cost), (C) partial evaluation: 2^4 kernel cofactors, then
+ * Shannon decompositions into 1024 / 4096 / 16384 / 32768 work-queue leaves;
+ * a plan whose predicted preparation alone exceeds the best total so far is
+ * skipped.  Every tried plan is prepared and timed for real (CUDA events on
+ * `stream`, best of 3); p's options are set to the plan of least total.
+ * Writes a JSON report (every plan with prep_s, ms and total_s or the reason
+ * it was skipped; the variant sweep's candidates; the choice) to report
+ * (nullable).  Results do not depend on the plan; only speed does.  Not
+ * thread-safe with other calls on the same program.  n < 24: no-op. */
 int bfa_autotune(bfa_prog* p, int n, void* stream, char* report, size_t len);
 
 /* As bfa_autotune, for later counts over aligned sub-cubes of 2^k_free

@@ -417,26 +417,47 @@ uint32_t gate_count(const Parsed& p) {
   return g;
 }
 
-std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total) {
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total, int threads) {
   std::vector<int> chosen;
   if (best_total) *best_total = UINT64_MAX;
+  threads = std::max(1, std::min(threads, 64));
   for (int step = 0; step < j; step++) {
-    int best_v = -1;
-    uint64_t best = UINT64_MAX;
-    for (int v = 0; v < k; v++) {
-      if (!((p.support_mask >> v) & 1) || std::find(chosen.begin(), chosen.end(), v) != chosen.end()) continue;
+    std::vector<int> cand;
+    for (int v = 0; v < k; v++)
+      if (((p.support_mask >> v) & 1) && std::find(chosen.begin(), chosen.end(), v) == chosen.end()) cand.push_back(v);
+    // total gates of the 2^(step+1) cofactors for each candidate (candidates
+    // in parallel when threads > 1; the choice -- least total, ties to the
+    // lowest variable -- does not depend on the thread count)
+    std::vector<uint64_t> total(cand.size(), 0);
+    auto score = [&](size_t ci) {
+      const int v = cand[ci];
       uint64_t mask = 1ull << v;
       for (int c : chosen) mask |= 1ull << c;
-      uint64_t total = 0;
-      for (uint64_t a = 0; a < (1ull << (chosen.size() + 1)) && total < best; a++) {
+      uint64_t t = 0;
+      for (uint64_t a = 0; a < (1ull << (chosen.size() + 1)); a++) {
         uint64_t values = 0;
         int bit = 0;
         for (int c : chosen) values |= ((a >> bit++) & 1) << c;
         values |= ((a >> bit) & 1) << v;
-        total += gate_count(assume(p, k, mask, values, nullptr));
+        t += gate_count(assume(p, k, mask, values, nullptr));
       }
-      if (total < best) { best = total; best_v = v; }
+      total[ci] = t;
+    };
+    if (threads == 1 || cand.size() < 2) {
+      for (size_t ci = 0; ci < cand.size(); ci++) score(ci);
+    } else {
+      std::atomic<size_t> next{0};
+      std::vector<std::thread> th;
+      for (int w = 0; w < std::min<int>(threads, (int)cand.size()); w++)
+        th.emplace_back([&] {
+          for (size_t ci; (ci = next.fetch_add(1)) < cand.size();) score(ci);
+        });
+      for (auto& x : th) x.join();
     }
+    int best_v = -1;
+    uint64_t best = UINT64_MAX;
+    for (size_t ci = 0; ci < cand.size(); ci++)
+      if (total[ci] < best) { best = total[ci]; best_v = cand[ci]; }
     if (best_v < 0) break;
     chosen.push_back(best_v);
     if (best_total) *best_total = best;
@@ -937,11 +958,11 @@ double model_cost(const Parsed& prog, const KernelSpec& spec) {
 // thread and outer positions; the smallest cones (variables outside the
 // support first) take the inner-loop positions, so most cells hoist out of
 // the inner loop.
-static std::vector<int8_t> constructive_roles(const Parsed& prog, const KernelSpec& spec, int k_free) {
+static std::vector<int8_t> constructive_roles(const Parsed& prog, const KernelSpec& spec, int k_free, int threads) {
   const int s = spec.slot_bits, t = spec.thread_bits, m = spec.inner_bits;
   std::vector<int8_t> pm(64);
   for (int v = 0; v < 64; v++) pm[v] = (int8_t)v;
-  std::vector<int> slot = choose_cofactor_vars(prog, k_free, std::max(0, std::min(s, k_free - 5)));
+  std::vector<int> slot = choose_cofactor_vars(prog, k_free, std::max(0, std::min(s, k_free - 5)), nullptr, threads);
   const Dag& d = prog.dag;
   std::vector<uint64_t> sup(d.nodes.size(), 0);
   std::vector<uint8_t> in_cone(d.nodes.size(), 0);
@@ -1032,7 +1053,7 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
   double best_c = 1e300;
   int evals = 0;
   {
-    std::vector<std::vector<int8_t>> cand{perm, constructive_roles(prog, base, k_free)};
+    std::vector<std::vector<int8_t>> cand{perm, constructive_roles(prog, base, k_free, threads)};
     const int R = std::max(0, std::min(budget / 16, budget - 2));
     for (int r = 0; r < R; r++) {
       std::vector<int8_t> pm = perm;
@@ -1046,17 +1067,19 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
       if (cost[r] < best_c) { best_c = cost[r]; best = cand[r]; }
     }
   }
-  // hill climbing: swap the positions of two variables of different role
-  // classes; candidates are drawn from the current point in sequence,
-  // evaluated speculatively in batches, and the first acceptable one (in
-  // draw order) is committed -- the generator is rewound to just after it
+  // hill climbing in rounds of kRound swap candidates (two variables of
+  // different role classes) drawn from the current point and evaluated
+  // together (in parallel when threads > 1): move to the best strictly
+  // improving one, else to the first equal-cost one (sideways moves cross
+  // plateaus).  The round size is fixed, so the result does not depend on
+  // the thread count.
+  constexpr int kRound = 8;
   std::vector<int8_t> cur = best;
   double cur_c = best_c;
   int stall = 0;
   while (evals < budget && stall < 100000) {
     std::vector<std::vector<int8_t>> cand;
-    std::vector<uint64_t> state_after;
-    const int B = std::min(threads, budget - evals);
+    const int B = std::min(kRound, budget - evals);
     while ((int)cand.size() < B && stall < 100000) {
       int a = (int)rnd((uint64_t)k_free), c = (int)rnd((uint64_t)k_free);
       if (role(cur[a]) == role(cur[c])) { stall++; continue; }
@@ -1064,20 +1087,21 @@ std::vector<int8_t> search_roles(const Parsed& prog, const KernelSpec& base, int
       std::vector<int8_t> pm = cur;
       std::swap(pm[a], pm[c]);
       cand.push_back(std::move(pm));
-      state_after.push_back(rs);
     }
     if (cand.empty()) break;
     std::vector<double> cost;
     eval_batch(cand, &cost);
-    for (size_t i = 0; i < cand.size(); i++) {
-      evals++;
-      if (cost[i] <= cur_c) {      // sideways moves too: walks across plateaus
-        cur_c = cost[i];
-        cur = cand[i];
-        if (cur_c < best_c) { best_c = cur_c; best = cur; }
-        rs = state_after[i];       // later candidates were drawn from the old point
-        break;
-      }
+    evals += (int)cand.size();
+    int pick = -1;
+    for (size_t i = 0; i < cand.size(); i++)
+      if (cost[i] < cur_c && (pick < 0 || cost[i] < cost[pick])) pick = (int)i;
+    if (pick < 0)
+      for (size_t i = 0; i < cand.size() && pick < 0; i++)
+        if (cost[i] == cur_c) pick = (int)i;
+    if (pick >= 0) {
+      cur = cand[pick];
+      cur_c = cost[pick];
+      if (cur_c < best_c) { best_c = cur_c; best = cur; }
     }
   }
   bool identity = true;
@@ -1526,14 +1550,31 @@ std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::
      << "\tsetp.le.u32 %p3, %qv, %c;\n\t@%p3 mov.u32 %lo, %mid;\n\t@!%p3 sub.u32 %hi, %mid, 1;\n\tbra.uni $Q_bs;\n"
      << "$Q_found:\n\tmul.wide.u32 %x, %lo, 4;\n\tmov.u64 %y, bfa_qpre;\n\tadd.u64 %x, %y, %x;\n"
      << "\tld.const.u32 %qv, [%x];\n\tsub.u32 %k, %c, %qv;\n\tbra.uni $Q_dispatch;\n";
+  const bool brx = getenv("BFA_PTX_BRX") != nullptr;  // debugging: indirect-branch dispatch
   for (size_t i = 0; i < nb; i++)
     os << "$Q_b" << i << ":\n\t{\n\t.param .b64 a0;\n\t.param .b32 a1;\n\t.param .b32 a2;\n"
        << "\tmov.u32 %s, " << chunks[i] << ";\n"
        << "\tst.param.b64 [a0], %cnt;\n\tst.param.b32 [a1], %k;\n\tst.param.b32 [a2], %s;\n"
        << "\tcall.uni " << body_name[i] << ", (a0, a1, a2);\n\t}\n\tbra.uni $Q_loop;\n";
-  os << "$Q_targets: .branchtargets ";
-  for (size_t i = 0; i < nb; i++) os << (i ? ", " : "") << "$Q_b" << i;
-  os << ";\n$Q_dispatch:\n\tbrx.idx.uni %lo, $Q_targets;\n}\n";
+  if (brx) {
+    os << "$Q_targets: .branchtargets ";
+    for (size_t i = 0; i < nb; i++) os << (i ? ", " : "") << "$Q_b" << i;
+    os << ";\n$Q_dispatch:\n\tbrx.idx.uni %lo, $Q_targets;\n}\n";
+    return os.str();
+  }
+  // dispatch: a balanced tree of uniform compare-and-branch on the body index
+  os << "$Q_dispatch:\n";
+  std::function<void(size_t, size_t, const std::string&)> tree = [&](size_t a, size_t b, const std::string& lbl) {
+    if (!lbl.empty()) os << lbl << ":\n";
+    if (b - a == 1) { os << "\tbra.uni $Q_b" << a << ";\n"; return; }
+    const size_t mid = (a + b) / 2;
+    const std::string right = "$Q_t" + std::to_string(mid) + "_" + std::to_string(b);
+    os << "\tsetp.ge.u32 %p3, %lo, " << mid << ";\n\t@%p3 bra.uni " << right << ";\n";
+    tree(a, mid, "");
+    tree(mid, b, right);
+  };
+  tree(0, nb, "");
+  os << "}\n";
   return os.str();
 }
 

@@ -90,7 +90,7 @@ uint32_t gate_count(const Parsed& p);
 
 // Kernel-level cofactoring: greedily pick j of the variables < k whose
 // 2^j cofactors (bfa_assume) have the fewest gates in total after Reduction.
-std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total = nullptr);
+std::vector<int> choose_cofactor_vars(const Parsed& p, int k, int j, uint64_t* best_total = nullptr, int threads = 1);
 
 // ---------------------------------------------------------------- mapping
 struct Lut {

@@ -315,6 +315,11 @@ constexpr int kPtxOptCount = 2;
 bool is_ptx_source(const std::string& src) { return src.compare(0, 28, "// generated by libbfa (PTX)") == 0; }
 
 int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
+  if (const char* dir = getenv("BFA_DUMP_SRC")) {  // debugging: keep every generated source
+    char path[4096];
+    snprintf(path, sizeof path, "%s/%016llx.ptx", dir, (unsigned long long)fnv64(ptx.data(), ptx.size()));
+    if (FILE* f = fopen(path, "w")) { fwrite(ptx.data(), 1, ptx.size(), f); fclose(f); }
+  }
   nvPTXCompilerHandle h = nullptr;
   nvPTXCompileResult r = nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str());
   if (r != NVPTXCOMPILE_SUCCESS) return set_err(BFA_E_JIT, "nvPTXCompilerCreate: %d", (int)r);
@@ -387,6 +392,7 @@ struct Options {
   int split_min_vars = 24;       // pieces with <= this many free variables are not split further
   int jit_cache = 1;             // 0: this program neither reads nor writes the persistent JIT cache
   int ptx = 1;                   // count-mode specialised kernels / work-queue modules emitted as PTX
+  int tune_counts = 1;           // bfa_autotune objective: preparation + tune_counts x count time
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -2229,6 +2235,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
   else if (k == "ptx") { if (v < 0 || v > 1) return bad(); p->opt.ptx = (int)v; }
+  else if (k == "tune_counts") { if (v < 1 || v > 1000000000) return bad(); p->opt.tune_counts = (int)v; }
   else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
   else if (k == "split_min_vars") { if (v < 5 || v > 63) return bad(); p->opt.split_min_vars = (int)v; }
   else return set_err(BFA_E_ARG, "unknown option '%s'", key);
@@ -2370,150 +2377,202 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     if (report && len) snprintf(report, len, "%s", js.str().c_str());
     return BFA_OK;
   }
-  // probe: the top 2^k valuations (k <= 36), the same launch planning as a real call
-  const int k = std::min(n, 36);
-  const uint64_t hi = n == 63 ? (1ull << 63) : (1ull << n), lo = hi - (1ull << k);
+  // Objective: the caller's total cost, preparation + tune_counts x count time
+  // over one 2^k_free sub-cube.  Every plan tried is prepared and timed for
+  // real (its preparation as measured here, JIT cache as the program's
+  // option says); a plan whose predicted preparation alone exceeds the best
+  // total so far is not tried.
+  const double K = (double)std::max(1, p->opt.tune_counts);
+  const int cores = (int)std::max(1u, std::thread::hardware_concurrency());
+  const uint64_t hi = n == 63 ? (1ull << 63) : (1ull << n), tlo = hi - (1ull << k_free);
   const Options base = p->opt;
-  struct Cand { Options o; double ms = -1; int regs = 0; uint32_t cells = 0; };
-  std::vector<Cand> cands;
-  for (int sb : {2, 3, 4, 5})
-    for (int ic : {0, 35, 50}) {
-      Cand c; c.o = base;
-      c.o.slot_bits = sb; c.o.inner_bits = 4;
-      c.o.dual_pipe = ic ? 1 : 0; c.o.imad_cost_pct = ic;
-      cands.push_back(c);
-    }
-  for (int sb : {3, 4}) {
-    Cand c; c.o = base;
-    c.o.slot_bits = sb; c.o.inner_bits = 2; c.o.dual_pipe = 1; c.o.imad_cost_pct = 50;
-    cands.push_back(c);
-  }
-  // occupancy for registers: cap at 128 (2 blocks of 256) or 168 (3 x 128)
-  for (int sb : {3, 4, 5}) {
-    Cand c; c.o = base;
-    c.o.slot_bits = sb; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35; c.o.min_blocks = 2;
-    cands.push_back(c);
-  }
-  {
-    Cand c; c.o = base;
-    c.o.slot_bits = 5; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35;
-    c.o.thread_bits = 7; c.o.min_blocks = 3;
-    cands.push_back(c);
-  }
-  // phase 1: compile every candidate's specialised kernel in parallel (host only)
-  std::vector<bfa::KernelSpec> specs(cands.size());
-  std::vector<int> ok(cands.size(), 0);
-  for (size_t i = 0; i < cands.size(); i++) {
-    const int T = 1 << cands[i].o.thread_bits;
-    const int full_grid = di.sms * std::max(1, cands[i].o.blocks_per_sm ? cands[i].o.blocks_per_sm : 2048 / T / 2);
-    std::vector<Segment> segs = plan(cands[i].o, cands[i].o.slot_bits, n, lo >> 5, hi >> 5, full_grid);
-    for (const Segment& sg : segs)
-      if (!sg.generic) {
-        bfa::KernelSpec& sp = specs[i];
-        sp.mode = bfa::KM_COUNT; sp.generic = false; sp.slot_bits = cands[i].o.slot_bits;
-        sp.thread_bits = cands[i].o.thread_bits; sp.inner_bits = sg.m; sp.dual_pipe = cands[i].o.dual_pipe;
-        sp.imad_cost_pct = cands[i].o.imad_cost_pct; sp.min_blocks = cands[i].o.min_blocks;
-        ok[i] = 1;
-      }
-  }
-  {
-    std::vector<std::thread> th;
-    std::vector<int> rcs(cands.size(), 0);
-    for (size_t i = 0; i < cands.size(); i++)
-      if (ok[i]) th.emplace_back([&, i] { g_worker = true; JitEntry* e = nullptr;
-                                          resolve_roles(p, &specs[i], k_free);
-                                          rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
-                                          if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner; });
-    for (auto& t : th) t.join();
-    for (size_t i = 0; i < cands.size(); i++)
-      if (ok[i] && rcs[i]) ok[i] = 0;
-  }
-  // phase 2: time each candidate on the probe (module load + 1 untimed launch, best of 3)
   uint64_t* d = nullptr;
   if ((rc = scratch_u64(dev, &d))) return rc;
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  int best = -1;
-  for (size_t i = 0; i < cands.size(); i++) {
-    if (!ok[i] || cands[i].cells > 8192) continue;  // i-cache: skip very long bodies
-    p->opt = cands[i].o;
-    if ((rc = run_range(p, n, lo, hi, nullptr, d, st, false, k_free))) { p->opt = base; return rc; }
-    float bestms = 1e30f;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto secs = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+  };
+  // prepare (first call) and time (best of 3 further calls) the current
+  // options over [lo, hi); returns the step in ms or < 0 on error
+  auto trial = [&](uint64_t lo, double* prep_s, int roles_k = -1) -> double {
+    const auto t0 = now();
+    int r2 = run_range(p, n, lo, hi, nullptr, d, st, false, roles_k);
+    if (r2 || cudaStreamSynchronize(st) != cudaSuccess) { rc = r2 ? r2 : set_err(BFA_E_CUDA, "autotune"); return -1; }
+    *prep_s = secs(t0, now());
+    float bm = 1e30f;
     for (int r = 0; r < 3; r++) {
       cudaEventRecord(e0, st);
-      run_range(p, n, lo, hi, nullptr, d, st, false, k_free);
+      run_range(p, n, lo, hi, nullptr, d, st, false, roles_k);
       cudaEventRecord(e1, st);
       cudaEventSynchronize(e1);
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
-      bestms = std::min(bestms, ms);
+      bm = std::min(bm, ms);
     }
-    cands[i].ms = bestms;
-    JitEntry* e = nullptr;
-    get_kernel(p, specs[i], dev, &e, nullptr);
-    cands[i].regs = e ? e->regs : 0;
-    if (best < 0 || cands[i].ms < cands[best].ms) best = (int)i;
+    return bm;
+  };
+  struct Plan {
+    std::string what;
+    Options o;
+    double prep = 0, ms = -1, total = 1e300;
+    std::string skipped;
+    Plan(std::string w, const Options& op) : what(std::move(w)), o(op) {}
+  };
+  std::vector<Plan> plans;
+  int best = -1;
+  auto consider = [&](Plan pl) {
+    if (pl.ms >= 0) {
+      pl.total = pl.prep + K * pl.ms / 1e3;
+      if (best < 0 || pl.total < plans[best].total) best = (int)plans.size();
+    }
+    plans.push_back(std::move(pl));
+  };
+  // ---- A: the current options as one exhaustive kernel (no partial evaluation)
+  p->opt.kernel_cofactor_bits = 0;
+  p->opt.split_pieces = 0;
+  {
+    Plan a{"exhaustive (current options)", p->opt};
+    a.ms = trial(tlo, &a.prep);
+    if (a.ms < 0) { p->opt = base; cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+    consider(a);
   }
-  cudaError_t ce = cudaStreamSynchronize(st);
-  if (ce != cudaSuccess) { p->opt = base; return set_err(BFA_E_CUDA, "autotune: %s", cudaGetErrorString(ce)); }
-  p->opt = best >= 0 ? cands[best].o : base;
-  // phase 3: partial evaluation (count mode over the whole sub-cube the
-  // caller will count: 2^k_free valuations when that takes <= ~2 s, else the
-  // probe).  Stage A: kernel-level cofactoring, 2^j cofactor kernels.  Stage
-  // Q: a Shannon decomposition into split_pieces leaves run as work-queue
-  // kernels of <= 512 bodies: 32768 leaves (C5: 4096 / 16384 / 32768 /
-  // 65536 leaves -> 5.1 / 2.2 / 1.3 / 1.4 ms), 16384 if that lost and
-  // prepared quickly; only when the whole count takes > 1 ms.
-  struct Trial { int sp, j, qb; float ms; double prep_s; };
-  std::vector<Trial> kcof;
-  if (best >= 0 && k_free >= 28) {
-    const double est = cands[best].ms * std::pow(2.0, k_free - k);
-    uint64_t tlo = lo, thi = hi;
-    if (est <= 2000.0 && k_free == n) { tlo = 0; thi = hi; }
-    else if (est <= 2000.0) { thi = hi; tlo = hi - (1ull << k_free); }
-    Trial bestt{0, 0, 0, 1e30f, 0};
-    auto trial = [&](int sp, int jj, int qb) -> int {
-      if (jj < 0 || jj > 8) return BFA_OK;
-      for (auto& done : kcof)
-        if (done.sp == sp && done.j == jj && done.qb == qb) return BFA_OK;
-      if (aligned_k(tlo >> 5, thi >> 5) < 24 + jj + (sp ? 4 : 0)) return BFA_OK;
-      p->opt.kernel_cofactor_bits = jj;
-      p->opt.split_pieces = sp;
-      p->opt.queue_bodies = qb;
-      const auto t0 = std::chrono::steady_clock::now();
-      int r2 = run_range(p, n, tlo, thi, nullptr, d, st, false);
-      if (r2) return r2;
-      cudaStreamSynchronize(st);
-      const double prep = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-      float bm = 1e30f;
-      for (int r = 0; r < 3; r++) {  // direct, graph capture + replay, replay
-        cudaEventRecord(e0, st);
-        run_range(p, n, tlo, thi, nullptr, d, st, false);
-        cudaEventRecord(e1, st);
-        cudaEventSynchronize(e1);
-        float ms = 0;
-        cudaEventElapsedTime(&ms, e0, e1);
-        bm = std::min(bm, ms);
+  const double prep_a = plans[0].prep, ms_a = plans[0].ms;
+  // ---- B: the kernel-variant sweep (slot bits, inner-loop bits, IMAD balance,
+  // register caps), compiled in parallel and timed on a probe of <= 2^36
+  // valuations; worth its cost only if a 30 % faster kernel repays it
+  const int kp = std::min(k_free, 36);
+  const uint64_t plo = hi - (1ull << kp);
+  struct Cand { Options o; double ms = -1; int regs = 0; uint32_t cells = 0; };
+  std::vector<Cand> cands;
+  {
+    const Options o0 = p->opt;
+    for (int sb : {2, 3, 4, 5})
+      for (int ic : {0, 35, 50}) {
+        Cand c; c.o = o0;
+        c.o.slot_bits = sb; c.o.inner_bits = 4;
+        c.o.dual_pipe = ic ? 1 : 0; c.o.imad_cost_pct = ic;
+        cands.push_back(c);
       }
-      kcof.push_back({sp, jj, qb, bm, prep});
-      if (bm < bestt.ms) bestt = kcof.back();
-      return BFA_OK;
-    };
-    for (int jj : {0, 4})
-      if ((rc = trial(0, jj, 0))) break;
-    if (!rc && bestt.ms > 1.0f) {
-      rc = trial(32768, 0, 512);
-      if (!rc && bestt.sp != 32768 && kcof.back().prep_s < 120.0) rc = trial(16384, 0, 512);
+    for (int sb : {3, 4}) {
+      Cand c; c.o = o0;
+      c.o.slot_bits = sb; c.o.inner_bits = 2; c.o.dual_pipe = 1; c.o.imad_cost_pct = 50;
+      cands.push_back(c);
     }
-    if (rc) p->opt = cands[best].o;
-    p->opt.kernel_cofactor_bits = bestt.j;
-    p->opt.split_pieces = bestt.sp;
-    p->opt.queue_bodies = bestt.qb;
+    for (int sb : {3, 4, 5}) {  // occupancy for registers: cap at 128 (2 blocks of 256)
+      Cand c; c.o = o0;
+      c.o.slot_bits = sb; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35; c.o.min_blocks = 2;
+      cands.push_back(c);
+    }
+    Cand c; c.o = o0;
+    c.o.slot_bits = 5; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35;
+    c.o.thread_bits = 7; c.o.min_blocks = 3;
+    cands.push_back(c);
   }
+  const double probe_ms = ms_a * std::ldexp(1.0, kp - k_free);
+  const double sweep_est = prep_a * (double)cands.size() / std::min<int>(cores, (int)cands.size()) * 1.5 +
+                           (double)cands.size() * 4.0 * probe_ms / 1e3;
+  if (K * ms_a / 1e3 * 0.3 <= sweep_est) {
+    Plan b{"kernel-variant sweep", p->opt};
+    char why[160];
+    snprintf(why, sizeof why, "predicted sweep %.2f s > 30%% of %g counts x %.1f ms", sweep_est, K, ms_a);
+    b.skipped = why;
+    plans.push_back(b);
+  } else {
+    const auto tb = now();
+    const Options o0 = p->opt;
+    std::vector<bfa::KernelSpec> specs(cands.size());
+    std::vector<int> ok(cands.size(), 0);
+    for (size_t i = 0; i < cands.size(); i++) {
+      const int T = 1 << cands[i].o.thread_bits;
+      const int full_grid = di.sms * std::max(1, cands[i].o.blocks_per_sm ? cands[i].o.blocks_per_sm : 2048 / T / 2);
+      for (const Segment& sg : plan(cands[i].o, cands[i].o.slot_bits, n, plo >> 5, hi >> 5, full_grid))
+        if (!sg.generic) {
+          bfa::KernelSpec& sp = specs[i];
+          sp.mode = bfa::KM_COUNT; sp.generic = false; sp.slot_bits = cands[i].o.slot_bits;
+          sp.thread_bits = cands[i].o.thread_bits; sp.inner_bits = sg.m; sp.dual_pipe = cands[i].o.dual_pipe;
+          sp.imad_cost_pct = cands[i].o.imad_cost_pct; sp.min_blocks = cands[i].o.min_blocks;
+          ok[i] = 1;
+        }
+    }
+    {  // compile every candidate in parallel (host only)
+      std::vector<int> rcs(cands.size(), 0);
+      parallel_for(cands.size(), [&](size_t i) {
+        if (!ok[i]) return;
+        JitEntry* e = nullptr;
+        resolve_roles(p, &specs[i], k_free);
+        rcs[i] = get_kernel(p, specs[i], -1, &e, nullptr);
+        if (!rcs[i]) cands[i].cells = e->stats.luts_inner + e->stats.imads_inner;
+      });
+      for (size_t i = 0; i < cands.size(); i++)
+        if (ok[i] && rcs[i]) ok[i] = 0;
+    }
+    int bc = -1;
+    for (size_t i = 0; i < cands.size(); i++) {   // time each on the probe
+      if (!ok[i] || cands[i].cells > 8192) continue;  // i-cache: skip very long bodies
+      p->opt = cands[i].o;
+      double pr = 0;
+      cands[i].ms = trial(plo, &pr, k_free);
+      if (cands[i].ms < 0) { p->opt = base; cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+      JitEntry* e = nullptr;
+      get_kernel(p, specs[i], dev, &e, nullptr);
+      cands[i].regs = e ? e->regs : 0;
+      if (bc < 0 || cands[i].ms < cands[bc].ms) bc = (int)i;
+    }
+    p->opt = bc >= 0 ? cands[bc].o : o0;
+    Plan b{"kernel-variant sweep winner", p->opt};
+    double pr = 0;
+    b.ms = trial(tlo, &pr);  // the winner over the whole sub-cube (its roles for k_free)
+    if (b.ms < 0) { p->opt = base; cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+    b.prep = secs(tb, now());
+    consider(b);
+    p->opt = plans[best].o;
+  }
+  // ---- C: partial evaluation (the Reduction at preparation time): 2^4
+  // kernel cofactors, then Shannon decompositions into work-queue leaves;
+  // preparation predicted from the previous trial (per piece), skipped when
+  // it alone exceeds the best total
+  const Options ob = plans[best].o;
+  double per_piece = -1;  // measured preparation seconds per decomposition leaf
+  if (k_free >= 28) {
+    struct T { int sp, j; };
+    for (T t : {T{0, 4}, T{1024, 0}, T{4096, 0}, T{16384, 0}, T{32768, 0}}) {
+      Plan c{t.sp ? "decomposed, " + std::to_string(t.sp) + " work-queue leaves" : "2^4 kernel cofactors", ob};
+      c.o.kernel_cofactor_bits = t.j;
+      c.o.split_pieces = t.sp;
+      c.o.queue_bodies = t.sp ? 512 : 0;
+      if (aligned_k(tlo >> 5, hi >> 5) < c.o.decompose_min_k && t.sp) continue;
+      const double pred = t.sp == 0 ? prep_a * 16.0 / std::min(16, cores)
+                                    : (per_piece > 0 ? per_piece : 40.0 * prep_a / std::max(1, cores)) * t.sp;
+      if (pred >= plans[best].total) {
+        char why[160];
+        snprintf(why, sizeof why, "predicted preparation %.1f s >= best total %.2f s", pred, plans[best].total);
+        c.skipped = why;
+        plans.push_back(c);
+        continue;
+      }
+      p->opt = c.o;
+      c.ms = trial(tlo, &c.prep);
+      if (c.ms < 0) { p->opt = base; cudaEventDestroy(e0); cudaEventDestroy(e1); return rc; }
+      if (t.sp) per_piece = c.prep / t.sp;
+      consider(c);
+    }
+  }
+  p->opt = plans[best].o;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  js << "{\"probe_valuations\": " << (hi - lo) << ", \"k_free\": " << k_free << ", \"candidates\": [";
+  js << "{\"tune_counts\": " << K << ", \"k_free\": " << k_free << ", \"plans\": [";
+  for (size_t i = 0; i < plans.size(); i++) {
+    const Plan& pl = plans[i];
+    js << (i ? ", " : "") << "{\"plan\": \"" << pl.what << "\", \"slot_bits\": " << pl.o.slot_bits
+       << ", \"imad_cost_pct\": " << pl.o.imad_cost_pct << ", \"split_pieces\": " << pl.o.split_pieces
+       << ", \"kernel_cofactor_bits\": " << pl.o.kernel_cofactor_bits;
+    if (!pl.skipped.empty()) js << ", \"skipped\": \"" << pl.skipped << "\"}";
+    else js << ", \"prep_s\": " << pl.prep << ", \"ms\": " << pl.ms << ", \"total_s\": " << pl.total << "}";
+  }
+  js << "], \"candidates\": [";
   bool first = true;
   for (size_t i = 0; i < cands.size(); i++) {
     if (cands[i].ms < 0) continue;
@@ -2523,15 +2582,12 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
        << ", \"ms\": " << cands[i].ms << ", \"regs\": " << cands[i].regs << ", \"cells\": " << cands[i].cells << "}";
     first = false;
   }
-  js << "], \"best\": {\"slot_bits\": " << p->opt.slot_bits << ", \"inner_bits\": " << p->opt.inner_bits
-     << ", \"imad_cost_pct\": " << p->opt.imad_cost_pct << ", \"dual_pipe\": " << p->opt.dual_pipe
-     << ", \"min_blocks\": " << p->opt.min_blocks << ", \"thread_bits\": " << p->opt.thread_bits
-     << ", \"kernel_cofactor_bits\": " << p->opt.kernel_cofactor_bits << ", \"split_pieces\": " << p->opt.split_pieces
-     << ", \"queue_bodies\": " << p->opt.queue_bodies << "}, \"partial_evaluation\": [";
-  for (size_t i = 0; i < kcof.size(); i++)
-    js << (i ? ", " : "") << "{\"split_pieces\": " << kcof[i].sp << ", \"j\": " << kcof[i].j << ", \"queue_bodies\": "
-       << kcof[i].qb << ", \"ms\": " << kcof[i].ms << ", \"prep_s\": " << kcof[i].prep_s << "}";
-  js << "]}";
+  const Options& o = p->opt;
+  js << "], \"best\": {\"plan\": \"" << plans[best].what << "\", \"slot_bits\": " << o.slot_bits << ", \"inner_bits\": "
+     << o.inner_bits << ", \"imad_cost_pct\": " << o.imad_cost_pct << ", \"dual_pipe\": " << o.dual_pipe
+     << ", \"min_blocks\": " << o.min_blocks << ", \"thread_bits\": " << o.thread_bits
+     << ", \"kernel_cofactor_bits\": " << o.kernel_cofactor_bits << ", \"split_pieces\": " << o.split_pieces
+     << ", \"queue_bodies\": " << o.queue_bodies << ", \"total_s\": " << plans[best].total << "}}";
   if (report && len) snprintf(report, len, "%s", js.str().c_str());
   return BFA_OK;
 }

@@ -490,13 +490,29 @@ def test_autotune_keeps_results():
     """bfa_autotune only changes speed: C4 still counts 130023 and a
     sub-cube vector still equals the oracle's after tuning."""
     text, n, expect = W.config("c4")
-    p = bfa.Program(text)
+    p = bfa.Program(text).set_option("tune_counts", 100000)   # many counts: every stage is worth trying
     rep = p.autotune(n)
     assert rep["best"] and len(rep["candidates"]) >= 6
+    assert all("skipped" not in x for x in rep["plans"][:2])
     assert p.count(n) == expect
     lo = (1 << 36) - (1 << 22)
     ow, oc = oracle.evaluate(text, n, lo, 1 << 36)
     assert np.array_equal(host(p.eval_range(n, lo, 1 << 36)), ow)
+
+
+def test_autotune_total_cost_objective():
+    """bfa_autotune minimises preparation + tune_counts x count time: for ONE
+    count of C5 the plan with minutes of preparation is never chosen (its
+    predicted preparation alone exceeds the best total), and the choice is
+    the plan of least total among those tried."""
+    text, n, _ = W.config("c5")
+    p = presets.apply(bfa.Program(text), presets.EXHAUSTIVE, tune_counts=1)
+    rep = p.autotune(n)
+    tried = [x for x in rep["plans"] if "skipped" not in x]
+    assert tried and rep["best"]["total_s"] == min(x["total_s"] for x in tried)
+    assert any("skipped" in x and x["split_pieces"] == 32768 for x in rep["plans"])
+    assert rep["best"]["total_s"] < 10
+    assert p.count(n) == presets.apply(bfa.Program(text), presets.EXHAUSTIVE).count(n)
 
 
 # ------------------------------------------------------------ NEXT-4
