@@ -1550,19 +1550,14 @@ std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::
      << "\tsetp.le.u32 %p3, %qv, %c;\n\t@%p3 mov.u32 %lo, %mid;\n\t@!%p3 sub.u32 %hi, %mid, 1;\n\tbra.uni $Q_bs;\n"
      << "$Q_found:\n\tmul.wide.u32 %x, %lo, 4;\n\tmov.u64 %y, bfa_qpre;\n\tadd.u64 %x, %y, %x;\n"
      << "\tld.const.u32 %qv, [%x];\n\tsub.u32 %k, %c, %qv;\n\tbra.uni $Q_dispatch;\n";
-  const bool brx = getenv("BFA_PTX_BRX") != nullptr;  // debugging: indirect-branch dispatch
   for (size_t i = 0; i < nb; i++)
     os << "$Q_b" << i << ":\n\t{\n\t.param .b64 a0;\n\t.param .b32 a1;\n\t.param .b32 a2;\n"
        << "\tmov.u32 %s, " << chunks[i] << ";\n"
        << "\tst.param.b64 [a0], %cnt;\n\tst.param.b32 [a1], %k;\n\tst.param.b32 [a2], %s;\n"
        << "\tcall.uni " << body_name[i] << ", (a0, a1, a2);\n\t}\n\tbra.uni $Q_loop;\n";
-  if (brx) {
-    os << "$Q_targets: .branchtargets ";
-    for (size_t i = 0; i < nb; i++) os << (i ? ", " : "") << "$Q_b" << i;
-    os << ";\n$Q_dispatch:\n\tbrx.idx.uni %lo, $Q_targets;\n}\n";
-    return os.str();
-  }
   // dispatch: a balanced tree of uniform compare-and-branch on the body index
+  // (an indirect `brx.idx` over a 512-entry .branchtargets table returned
+  // wrong, run-to-run varying counts on sm_100a; the tree is exact)
   os << "$Q_dispatch:\n";
   std::function<void(size_t, size_t, const std::string&)> tree = [&](size_t a, size_t b, const std::string& lbl) {
     if (!lbl.empty()) os << lbl << ":\n";

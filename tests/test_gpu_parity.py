@@ -453,6 +453,45 @@ def test_count_shard_sums_to_count():
         assert a + b == 1 << n, world
 
 
+def test_decomposed_large_modules_vs_oracle():
+    """Work-queue modules of up to 512 bodies each (the bench preset's module
+    size) on an oracle-checkable sub-cube: a 2^26 C5 sub-cube decomposed into
+    leaves of >= 15 variables, bodies of 32 threads, counted against the
+    oracle over direct / captured / replayed calls."""
+    text, n, _ = W.config("c5")
+    base = bfa.Program(text)
+    rng = np.random.default_rng(7)
+    while True:
+        lo = int(rng.integers(0, 1 << (n - 26))) << 26
+        q, _, _ = base.assume(n, {v: (lo >> v) & 1 for v in range(26, n)})
+        if q.info["const_value"] == -1 and q.info["gates"] >= 300:
+            break
+    p = presets.apply(bfa.Program(text), presets.DECOMPOSED, thread_bits=5, split_pieces=2048, split_min_vars=15,
+                      decompose_min_k=24, queue_inner=0)
+    expect = oracle.count(text, n, lo, lo + (1 << 26))
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(4):
+        p.count_range(n, lo, lo + (1 << 26), out=out)
+        assert int(out.item()) == expect
+    q = bfa.last_launch()["queue"]
+    assert q["bodies"] >= 512 and q["modules"] <= -(-q["bodies"] // 16), q
+
+
+def test_decomposed_bench_preset_full_cube():
+    """The bench's replay configuration itself (presets.DECOMPOSED: 32768
+    Shannon leaves in work-queue modules of <= 512 bodies) over the whole C5
+    cube equals the oracle-checked exhaustive kernel's count, replay after
+    replay, and f + ~f covers the cube on the exhaustive side (P-11)."""
+    text, n, _ = W.config("c5")
+    ref = presets.apply(bfa.Program(text), presets.EXHAUSTIVE).count(n)
+    p = presets.apply(bfa.Program(text), presets.DECOMPOSED)
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    for _ in range(5):
+        p.count_range(n, 0, 1 << n, out=out)
+        assert int(out.item()) == ref
+    assert bfa.last_launch()["queue"]["bodies"] == 32768
+
+
 def test_concurrent_counts_on_two_streams():
     """One prepared decomposed C5 program counted on two streams at once
     (work-queue chunk counters are per caller stream and zeroed by every
