@@ -393,6 +393,7 @@ struct Options {
   int jit_cache = 1;             // 0: this program neither reads nor writes the persistent JIT cache
   int ptx = 1;                   // count-mode specialised kernels / work-queue modules emitted as PTX
   int tune_counts = 1;           // bfa_autotune objective: preparation + tune_counts x count time
+  int queue_light_pct = 15;      // light-tail leaves (<= this % of the work): 2^(s-2) slots, budget / 4
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -1067,7 +1068,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct;
   return k.str();
 }
 
@@ -1657,12 +1658,33 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
   };
   std::vector<Body> B(elig.size());
   std::atomic<size_t> n_reduced{0};
+  // the light tail: the lightest leaves that together hold <= queue_light_pct
+  // percent of the estimated work ((gates + 1) x 2^vars) get 2^(s-2) slots
+  // and a quarter of the role-search budget -- a quarter of the code to
+  // compile, for leaves whose run time hardly matters
+  std::vector<uint8_t> light(elig.size(), 0);
+  if (o.queue_light_pct > 0) {
+    std::vector<std::pair<double, size_t>> w;
+    double tot = 0;
+    for (size_t e = 0; e < elig.size(); e++) {
+      const double x = (double)(kids[elig[e]]->info.gates + 1) * std::ldexp(1.0, kids[elig[e]]->piece_nv);
+      w.push_back({x, e});
+      tot += x;
+    }
+    std::stable_sort(w.begin(), w.end());
+    double run = 0;
+    for (auto& x : w) {
+      run += x.first;
+      if (run > tot * o.queue_light_pct / 100.0) break;
+      light[x.second] = 1;
+    }
+  }
   parallel_for(elig.size(), [&](size_t e) {
     const size_t i = elig[e];
     bfa_prog* q = kids[i].get();
     Body& b = B[e];
     b.nv = q->piece_nv;
-    b.s = s;
+    b.s = light[e] ? std::max(0, s - 2) : s;
     // support reduction: a variable outside the leaf's support does not change
     // it, so the count over 2^nv valuations is 2^(nv-k) x the count over the k
     // kept ones; keep the support plus the lowest other variables up to
@@ -1700,7 +1722,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     // a leaf's kernel runs once per step while its role search runs once per
     // preparation: work-queue bodies search longer (C5, 32768 leaves: budget
     // 200 -> 1.31 ms, 400 -> 1.20 ms)
-    const_cast<bfa_prog*>(src)->opt.role_budget = o.queue_role_budget;
+    const_cast<bfa_prog*>(src)->opt.role_budget = light[e] ? std::max(16, o.queue_role_budget / 4) : o.queue_role_budget;
     resolve_roles(src, &spec, b.nv);
     b.name = "bfa_body_" + std::to_string(i);
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
@@ -2235,6 +2257,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
   else if (k == "ptx") { if (v < 0 || v > 1) return bad(); p->opt.ptx = (int)v; }
+  else if (k == "queue_light_pct") { if (v < 0 || v > 100) return bad(); p->opt.queue_light_pct = (int)v; }
   else if (k == "tune_counts") { if (v < 1 || v > 1000000000) return bad(); p->opt.tune_counts = (int)v; }
   else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
   else if (k == "split_min_vars") { if (v < 5 || v > 63) return bad(); p->opt.split_min_vars = (int)v; }
