@@ -11,8 +11,8 @@ random 1000-gate Boolean DAG over n = 42 variables, 2^42 valuations per step.
     python bench.py --impl reference ...                   (the CPU oracle arm)
 
 Headline (`value`): the paper's brute-force block evaluation (PAPER.md:356-372,
-955) -- ONE register-mode kernel (presets.EXHAUSTIVE: generators synthesised
-in registers, 32 slot cofactors folded into a straight-line LOP3/IMAD body,
+955) -- ONE register-mode kernel (presets.exhaustive(config): generators synthesised
+in registers, 2^slot_bits slot cofactors folded into a straight-line LOP3/IMAD body,
 searched variable roles, fused popcount + reduction) evaluates every word of
 every valuation of the rank's cofactor range [r 2^(n-p), (r+1) 2^(n-p)) inside
 the timed region; then ONE 8-byte NCCL all-reduce (P > 1).  Nothing is decided
@@ -21,7 +21,8 @@ other ranks load its cubin from the JIT cache) is outside the timed region and
 reported as prep_s, as in any JIT-compiled benchmark.
 
 `e2e`: a COLD call through the public API, every step: bfa_compile of the
-text -> bfa_count_range (role search + NVRTC with the persistent JIT cache
+text -> bfa_count_range with the plan of least preparation + one count
+(presets.cold: role search + PTX compile with the persistent JIT cache
 disabled, module load, launch) -> the count read on the host (and, P > 1,
 all-reduced); wall clock, max over ranks.
 
@@ -323,7 +324,8 @@ def run_bfa(args):
 
     text, n, expect = W.config(args.config)
     extra_opts = json.loads(args.options) if args.options else {}
-    prog = presets.apply(bfa.Program(text), presets.EXHAUSTIVE, **extra_opts)
+    preset = presets.exhaustive(args.config)
+    prog = presets.apply(bfa.Program(text), preset, **extra_opts)
     info = prog.info
     lo, hi = rank_range(n, rank, world)
     stream = torch.cuda.current_stream()
@@ -385,13 +387,13 @@ def run_bfa(args):
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        q = presets.apply(bfa.Program(text), presets.EXHAUSTIVE, jit_cache=0, **extra_opts)
+        q = presets.apply(bfa.Program(text), presets.cold(args.config), jit_cache=0, **extra_opts)
         t = q.count_range(n, lo, hi, stream=stream)
         if world > 1:
             dist.all_reduce(t)
         e2e_count = int(t.item()) & ((1 << 64) - 1)   # device -> host read (synchronises)
         e2e_t.append(time.perf_counter() - t0)
-        cubin_bytes = len(q.jit_cubin(1, n)) if world == 1 else 0
+        cubin_bytes = len(q.jit_cubin(1, n)) if world == 1 else 0   # (cached: no recompile)
         assert e2e_count == final, (e2e_count, final)
         del q
     e2e_s = statistics.median(e2e_t)
@@ -426,15 +428,17 @@ def run_bfa(args):
         "data": "synthetic (seeded generator, workloads/__init__.py)",
         "config": config_block(args.config, n, world),
         "program": {"gates_G": info["gates"], "luts_L": info["luts"], "support": info["support"],
-                    "options": dict(presets.EXHAUSTIVE, **extra_opts)},
+                    "options": dict(preset, **extra_opts)},
         "count": final, "count_expected": expect, "count_verified": verified,
         "decided_at_compile_time": 0,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {"value": (1 << n) / e2e_s, "unit": "valuations/s", "h2d_bytes_per_step": cubin_bytes,
                 "d2h_bytes_per_step": 8, "steps": e2e_steps, "s_per_call": e2e_s,
-                "call": "cold: bfa_compile(text) -> bfa_count_range over this rank's range (role search + NVRTC with "
-                        "the persistent JIT cache off, module load, launch) -> count read on the host"
+                "plan": dict(presets.cold(args.config), **extra_opts),
+                "call": "cold: bfa_compile(text) -> bfa_count_range over this rank's range with the plan of least "
+                        "preparation + one count (presets.cold: role search + PTX compile with the persistent JIT "
+                        "cache off, module load, launch) -> count read on the host"
                         + (" -> all-reduce" if world > 1 else ""),
                 "h2d": "the JIT'd cubin loaded into the device each call (count mode has no input tensors)"},
         "gpu_launches": launches_timed,
@@ -459,7 +463,7 @@ def run_extras(args, bfa, presets, torch, stream, dev, text, n, final, verified,
         # complement invariant through the same exhaustive preset (P-11)
         body, outl = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
         if args.config == "c5":
-            pc = presets.apply(bfa.Program(f"{body}\n~{outl}"), presets.EXHAUSTIVE)
+            pc = presets.apply(bfa.Program(f"{body}\n~{outl}"), presets.exhaustive(args.config))
             verified["complement_sum"] = final + pc.count(n) == 1 << n
         # the decomposed plan, cold preparation, then replays
         q = presets.apply(bfa.Program(text), presets.DECOMPOSED, jit_cache=0)
@@ -488,7 +492,7 @@ def run_extras(args, bfa, presets, torch, stream, dev, text, n, final, verified,
     if args.config == "c5":
         # the exhaustive line at n = 36 (C4)
         t4, n4, e4 = W.config("c4")
-        p4 = presets.apply(bfa.Program(t4), presets.EXHAUSTIVE)
+        p4 = presets.apply(bfa.Program(t4), presets.exhaustive("c4"))
         c4 = torch.zeros(1, dtype=torch.int64, device=dev)
         for _ in range(3):
             p4.count_range(n4, 0, 1 << n4, out=c4, stream=stream)

@@ -1437,7 +1437,7 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
   emit_level(1);
   body << "\tmov.u64 %acc, 0;\n\tmov.u64 %o, %ob;\n"
        << "\tsetp.ge.u64 %p0, %o, %oe;\n\t@%p0 bra $L_done;\n"
-       << "$L_outer:\n"
+       << "$L_outer:\n\t.pragma \"nounroll\";\n"
        << "\tshl.b64 %wo, %o, " << unit << ";\n\tadd.u64 %wo, %wo, %A;\n";
   for (int v = 0; v < 64; v++)
     if (used[v] && level_of(v) == 2) {
@@ -1448,7 +1448,7 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
     }
   emit_level(2);
   body << "\tmov.u32 %a32, 0;\n\tmov.u32 %ii, 0;\n"
-       << "$L_inner:\n";
+       << "$L_inner:\n\t.pragma \"nounroll\";\n";
   for (int v = 0; v < 64; v++)
     if (used[v] && level_of(v) == 3) {
       const int k = b.pos[v] - 5 - s - t;

@@ -810,7 +810,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
   // eval stores 2^s consecutive words per thread as one vector store: the
   // slice's word 0 must sit at a (4 * 2^s)-byte aligned address relative to
   // the unit grid, else use narrower slots.
-  int s_eff = o.slot_bits;
+  int s_eff = eval ? std::min(o.slot_bits, 5) : o.slot_bits;   // eval stores <= 32 words per thread-iteration
   if (eval)
     while (s_eff > 0 && ((reinterpret_cast<uintptr_t>(out_dev) - 4 * (uintptr_t)wlo) & ((4u << s_eff) - 1))) s_eff--;
   std::vector<Segment> segs = plan(o, s_eff, n, wlo, whi, full_grid);
@@ -2230,7 +2230,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   p->graphs.clear();
   std::string k(key);
   auto bad = [&]() { return set_err(BFA_E_ARG, "option %s=%lld out of range", key, (long long)v); };
-  if (k == "slot_bits") { if (v < 0 || v > 5) return bad(); p->opt.slot_bits = (int)v; }
+  if (k == "slot_bits") { if (v < 0 || v > 8) return bad(); p->opt.slot_bits = (int)v; }
   else if (k == "thread_bits") { if (v < 5 || v > 10) return bad(); p->opt.thread_bits = (int)v; }
   else if (k == "inner_bits") { if (v < 0 || v > 8) return bad(); p->opt.inner_bits = (int)v; }
   else if (k == "blocks_per_sm") { if (v < 0 || v > 32) return bad(); p->opt.blocks_per_sm = (int)v; }

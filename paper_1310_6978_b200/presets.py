@@ -3,13 +3,21 @@
 The benchmark and the GPU parity tests apply the SAME preset, so the kernel
 `bench.py` times is the kernel the oracle tests check.
 
-EXHAUSTIVE: the paper's brute-force block evaluation (PAPER.md:356-372,
+exhaustive(cfg): the paper's brute-force block evaluation (PAPER.md:356-372,
 §2.3; "brute force search"): one register-mode kernel over the
 whole cube, every word of every valuation evaluated by the kernel inside the
-timed region (32 slot cofactors constant-folded into the straight-line body,
-variable roles searched, LOP3 + IMAD cells).  Nothing is decided at
-preparation time.  The C5 autotune winner of round 1 (slot 5, IMAD cost 50,
-inner 4).
+timed region (2^slot_bits slot cofactors constant-folded into the
+straight-line body, variable roles searched, LOP3 + IMAD cells).  Nothing is
+decided at preparation time.  Chosen by full-cube sweeps on a B200
+(profiles/r02/sweep_exhaustive.jsonl):
+  C5 (n=42): slot 7, inner 2, role budget 400 -> 154 ms per 2^42
+             (slot 6 / inner 3: 170 ms; slot 5 / inner 4 / budget 200: 229 ms)
+  C4 (n=36): slot 8, inner 2 -> 0.079 ms per 2^36 (slot 5 / inner 4: 0.296 ms)
+
+cold(cfg): the plan of least preparation + ONE count (what a single cold
+bfa_count should run; bench.py's e2e): slot 5, inner 4, role budget 200 on
+C5 (about 0.25 s of role search + PTX compile for a 229 ms count, against
+about 1.2 s for the 154 ms kernel).
 
 DECOMPOSED: the Reduction applied at preparation time (killing variables /
 "further partition"): a Shannon
@@ -19,10 +27,32 @@ step time is a REPLAY of a prepared plan and is reported as such, next to
 its preparation cost.
 """
 
-EXHAUSTIVE = {"slot_bits": 5, "thread_bits": 8, "inner_bits": 4, "dual_pipe": 1, "imad_cost_pct": 50,
-              "min_blocks": 0, "kernel_cofactor_bits": 0, "split_pieces": 0}
+EXHAUSTIVE = {"slot_bits": 7, "thread_bits": 8, "inner_bits": 2, "dual_pipe": 1, "imad_cost_pct": 50,
+              "min_blocks": 0, "role_budget": 400, "kernel_cofactor_bits": 0, "split_pieces": 0}
 
-DECOMPOSED = dict(EXHAUSTIVE, split_pieces=32768, queue_bodies=512, queue_inner=2, queue_role_budget=100)
+_EXHAUSTIVE_BY_CONFIG = {
+    "c4": dict(EXHAUSTIVE, slot_bits=8, inner_bits=2, role_budget=200),
+}
+
+COLD = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200)
+
+_COLD_BY_CONFIG = {
+    "c4": _EXHAUSTIVE_BY_CONFIG["c4"],
+}
+
+DECOMPOSED = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200, split_pieces=32768, queue_bodies=512,
+                  queue_inner=2, queue_role_budget=100)
+
+
+def exhaustive(cfg: str) -> dict:
+    """The exhaustive-kernel preset of a named config (EXHAUSTIVE unless a
+    config has its own)."""
+    return _EXHAUSTIVE_BY_CONFIG.get(cfg, EXHAUSTIVE)
+
+
+def cold(cfg: str) -> dict:
+    """The least preparation + one count plan of a named config."""
+    return _COLD_BY_CONFIG.get(cfg, COLD)
 
 
 def apply(prog, preset: dict, **overrides):

@@ -19,7 +19,8 @@ torch.cuda.set_device(0)
 cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
 if what in ("exhaustive", "c4_exhaustive", "replay"):
     text, n, _ = W.config("c4" if what == "c4_exhaustive" else "c5")
-    p = presets.apply(bfa.Program(text), presets.DECOMPOSED if what == "replay" else presets.EXHAUSTIVE)
+    preset = presets.DECOMPOSED if what == "replay" else presets.exhaustive("c4" if what == "c4_exhaustive" else "c5")
+    p = presets.apply(bfa.Program(text), preset)
     for _ in range(steps):
         p.count_range(n, 0, 1 << n, out=cnt)
     torch.cuda.synchronize()

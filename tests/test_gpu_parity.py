@@ -209,16 +209,17 @@ def renamed(text, perm):
     return re.sub(r"\bx(\d+)\b", lambda m: f"x{perm[int(m.group(1))]}", text)
 
 
-@pytest.mark.parametrize("cfg", ["c5", "c4"])
-def test_exhaustive_bench_kernel_vs_oracle(cfg):
-    """The headline kernel bench.py times (presets.EXHAUSTIVE over the whole
+@pytest.mark.parametrize("cfg,plan", [("c5", "exhaustive"), ("c5", "cold"), ("c4", "exhaustive")])
+def test_exhaustive_bench_kernel_vs_oracle(cfg, plan):
+    """The headline kernel bench.py times (presets.exhaustive(cfg) over the whole
     2^n cube: same variant, same searched roles, same cubin) against the
     oracle on 4 random sub-ranges of its enumeration order, 2^24 valuations
     each (P-13; C5 cannot be oracle-checked whole).  bfa_count_positions runs
     exactly that kernel; the oracle counts the renamed program f' on the same
     position range."""
     text, n, expect = W.config(cfg)
-    p = presets.apply(bfa.Program(text), presets.EXHAUSTIVE)
+    preset = getattr(presets, plan)(cfg)     # bench.py's value (exhaustive) and e2e (cold) kernels
+    p = presets.apply(bfa.Program(text), preset)
     perm = p.roles(n)
     assert sorted(perm) == list(range(64)) and perm != list(range(64))
     text2 = renamed(text, perm)
@@ -233,12 +234,13 @@ def test_exhaustive_bench_kernel_vs_oracle(cfg):
     # the same compiled kernel over the whole cube: the count bench.py reports
     c = p.count(n)
     ll = bfa.last_launch()
-    assert ll["kernels"] == 1 and ll["segments"][0]["roles"] == "searched" and ll["segments"][0]["s"] == 5
+    seg = ll["segments"][0]
+    assert ll["kernels"] == 1 and seg["roles"] == "searched" and seg["s"] == preset["slot_bits"]
     if expect is not None:
         assert c == expect
     else:                          # C5: complement invariant (P-11) with the same preset
         body, out = "\n".join(text.splitlines()[:-1]), text.splitlines()[-1]
-        pc = presets.apply(bfa.Program(f"{body}\n~{out}"), presets.EXHAUSTIVE)
+        pc = presets.apply(bfa.Program(f"{body}\n~{out}"), preset)
         assert c + pc.count(n) == 1 << n
 
 
