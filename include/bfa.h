@@ -137,6 +137,8 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "split_merge"   > 0: after a split_pieces decomposition, merge sibling
  *                   leaves of <= this many gates each back into their parent
  *                   (default 0)
+ *   "queue_opt_level" ptxas optimisation level (0..3) of work-queue modules
+ *                   (default 3)
  *   "queue_light_pct" the lightest work-queue leaves holding <= this percent of
  *                   the estimated work get 2^(slot_bits-2) slots and a quarter
  *                   of the role-search budget (default 15; 0 = off)

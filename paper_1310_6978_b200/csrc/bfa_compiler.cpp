@@ -1517,10 +1517,11 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
 }
 
 std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::vector<std::string>& body_name,
-                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks) {
+                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks, int opt_level) {
   std::ostringstream os;
   const size_t nb = body_name.size();
-  os << "// generated by libbfa (PTX): work-queue kernel of " << nb << " programs\n" << kPtxHeader;
+  os << "// generated by libbfa (PTX) -O" << opt_level << ": work-queue kernel of " << nb << " programs\n"
+     << kPtxHeader;
   uint64_t total = 0;
   os << ".const .align 4 .u32 bfa_qpre[" << nb + 1 << "] = {";
   for (size_t i = 0; i < nb; i++) {

@@ -198,7 +198,7 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
 // the distinct bodies' .func text, body_name[i] / chunks[i] the body and
 // chunk count of queue entry i.
 std::string emit_ptx_queue(const std::vector<std::string>& body_ptx, const std::vector<std::string>& body_name,
-                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks);
+                           const std::vector<uint32_t>& chunks, int thread_bits, int min_blocks, int opt_level = 3);
 
 // CUDA C++ source of one kernel variant (entry point "bfa_kernel").
 std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats* stats);

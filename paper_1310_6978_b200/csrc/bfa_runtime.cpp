@@ -309,10 +309,21 @@ std::string cubin_cache_key(const std::string& src) {
 
 // Generated PTX (count-mode kernels, emit_ptx) goes straight to the PTX
 // compiler -- no C++ front end.
-const char* const kPtxOpts[] = {"--gpu-name=sm_100a", "-O3"};
+const char* const kPtxOpts[] = {"--gpu-name=sm_100a", "-O3"};  // [1]: the default level (ptx_opt)
 constexpr int kPtxOptCount = 2;
 
 bool is_ptx_source(const std::string& src) { return src.compare(0, 28, "// generated by libbfa (PTX)") == 0; }
+
+// A generated PTX module may ask for a lower ptxas optimisation level in its
+// first line ("// generated by libbfa (PTX) -O<k>: ..."); default -O3.
+const char* ptx_opt(const std::string& src) {
+  static const char* lv[] = {"-O0", "-O1", "-O2", "-O3"};
+  const size_t at = src.find('\n');
+  const size_t o = src.find(" -O", 0);
+  if (o != std::string::npos && o < at && o + 3 < src.size() && src[o + 3] >= '0' && src[o + 3] <= '3')
+    return lv[src[o + 3] - '0'];
+  return "-O3";
+}
 
 int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
   if (const char* dir = getenv("BFA_DUMP_SRC")) {  // debugging: keep every generated source
@@ -323,7 +334,8 @@ int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
   nvPTXCompilerHandle h = nullptr;
   nvPTXCompileResult r = nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str());
   if (r != NVPTXCOMPILE_SUCCESS) return set_err(BFA_E_JIT, "nvPTXCompilerCreate: %d", (int)r);
-  r = nvPTXCompilerCompile(h, kPtxOptCount, kPtxOpts);
+  const char* opts[] = {kPtxOpts[0], ptx_opt(ptx)};
+  r = nvPTXCompilerCompile(h, 2, opts);
   if (r != NVPTXCOMPILE_SUCCESS) {
     size_t n = 0;
     nvPTXCompilerGetErrorLogSize(h, &n);
@@ -394,6 +406,7 @@ struct Options {
   int ptx = 1;                   // count-mode specialised kernels / work-queue modules emitted as PTX
   int tune_counts = 1;           // bfa_autotune objective: preparation + tune_counts x count time
   int queue_light_pct = 15;      // light-tail leaves (<= this % of the work): 2^(s-2) slots, budget / 4
+  int queue_opt_level = 3;       // ptxas -O level of work-queue modules
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
 };
@@ -1068,7 +1081,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level;
   return k.str();
 }
 
@@ -1812,7 +1825,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
       std::vector<std::string> distinct;
       for (auto& x : bsrc)
         if (!x.empty()) distinct.push_back(std::move(x));
-      srcs.push_back(bfa::emit_ptx_queue(distinct, bname, ch, t, o.min_blocks));
+      srcs.push_back(bfa::emit_ptx_queue(distinct, bname, ch, t, o.min_blocks, o.queue_opt_level));
     } else {
       srcs.push_back(bfa::emit_queue(bsrc, bname, O, ch, t, o.min_blocks));
     }
@@ -2257,6 +2270,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "queue_chunk") { if (v < 1 || v > (1 << 24)) return bad(); p->opt.queue_chunk = (int)v; }
   else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
   else if (k == "ptx") { if (v < 0 || v > 1) return bad(); p->opt.ptx = (int)v; }
+  else if (k == "queue_opt_level") { if (v < 0 || v > 3) return bad(); p->opt.queue_opt_level = (int)v; }
   else if (k == "queue_light_pct") { if (v < 0 || v > 100) return bad(); p->opt.queue_light_pct = (int)v; }
   else if (k == "tune_counts") { if (v < 1 || v > 1000000000) return bad(); p->opt.tune_counts = (int)v; }
   else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
