@@ -141,7 +141,8 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   (default 3)
  *   "queue_light_pct" the lightest work-queue leaves holding <= this percent of
  *                   the estimated work get 2^(slot_bits-2) slots and a quarter
- *                   of the role-search budget (default 15; 0 = off)
+ *                   of the role-search budget (default 0 = off)
+ *   "queue_slot_bits" slot bits of work-queue bodies (-1 = slot_bits; default -1)
  *   "tune_counts"   bfa_autotune's objective: preparation + tune_counts x the
  *                   time of one count (default 1)
  *   "ptx"           1: count-mode specialised kernels and work-queue modules

@@ -405,7 +405,8 @@ struct Options {
   int jit_cache = 1;             // 0: this program neither reads nor writes the persistent JIT cache
   int ptx = 1;                   // count-mode specialised kernels / work-queue modules emitted as PTX
   int tune_counts = 1;           // bfa_autotune objective: preparation + tune_counts x count time
-  int queue_light_pct = 15;      // light-tail leaves (<= this % of the work): 2^(s-2) slots, budget / 4
+  int queue_light_pct = 0;       // light-tail leaves (<= this % of the work): 2^(s-2) slots, budget / 4
+  int queue_slot_bits = -1;      // slot bits of work-queue bodies (-1: slot_bits)
   int queue_opt_level = 3;       // ptxas -O level of work-queue modules
   int queue_support = 0;         // 1: work-queue bodies enumerate only their support (count scaled;
                                  // measured slower on C5: 2.00 vs 1.31 ms, the reduced bodies lose hoisting)
@@ -1081,7 +1082,7 @@ std::string options_key(const Options& o) {
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
     << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
-    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level;
+    << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level << ',' << o.queue_slot_bits;
   return k.str();
 }
 
@@ -1649,7 +1650,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     if (it != holder->queues.end()) { *out = &it->second; return BFA_OK; }
   }
   const Options& o = holder->opt;
-  const int s = o.slot_bits, t = o.thread_bits;
+  const int s = o.queue_slot_bits >= 0 ? o.queue_slot_bits : o.slot_bits, t = o.thread_bits;
   std::vector<size_t> elig;
   for (size_t i = 0; i < kids.size(); i++) {
     const bfa_prog* q = kids[i].get();
@@ -2271,6 +2272,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "jit_cache") { if (v < 0 || v > 1) return bad(); p->opt.jit_cache = (int)v; }
   else if (k == "ptx") { if (v < 0 || v > 1) return bad(); p->opt.ptx = (int)v; }
   else if (k == "queue_opt_level") { if (v < 0 || v > 3) return bad(); p->opt.queue_opt_level = (int)v; }
+  else if (k == "queue_slot_bits") { if (v < -1 || v > 8) return bad(); p->opt.queue_slot_bits = (int)v; }
   else if (k == "queue_light_pct") { if (v < 0 || v > 100) return bad(); p->opt.queue_light_pct = (int)v; }
   else if (k == "tune_counts") { if (v < 1 || v > 1000000000) return bad(); p->opt.tune_counts = (int)v; }
   else if (k == "decompose_min_k") { if (v < 10 || v > 64) return bad(); p->opt.decompose_min_k = (int)v; }
