@@ -109,6 +109,9 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *   "role_search"   1 = count mode searches the variable -> bit-position roles on
  *                   aligned sub-cubes of >= 2^24 valuations (default 1)
  *   "role_budget"   model evaluations of that search (default 200)
+ *   "role_seeds"    independent searches (different seeds) of role_budget
+ *                   each; the permutation of least modelled cost is kept
+ *                   (default 1)
  *   "segment_cells" programs whose cover exceeds 8000 LUTs run as segments of
  *                   this many cells (0 = auto: 768), values crossing segments in
  *                   HBM slot arrays

@@ -387,6 +387,7 @@ struct Options {
   int min_blocks = 0;
   int role_search = 1;
   int role_budget = 200;
+  int role_seeds = 1;            // independent role searches, best modelled cost kept
   int segment_cells = 0;   // 0: auto (segment when L > 8000), > 0: always, this many cells
   int segment_remat = 2;   // recompute shared cells with cones <= this many cells
   int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
@@ -499,7 +500,8 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
   bfa_prog* p = const_cast<bfa_prog*>(cp);
   spec->perm.clear();
   if (!p->opt.role_search || spec->generic || spec->materialised || spec->mode != bfa::KM_COUNT || k_free < 24) return;
-  const std::string key = spec_key(*spec) + "k" + std::to_string(k_free) + "r" + std::to_string(p->opt.role_budget);
+  const std::string key = spec_key(*spec) + "k" + std::to_string(k_free) + "r" + std::to_string(p->opt.role_budget) +
+                          (p->opt.role_seeds > 1 ? "s" + std::to_string(p->opt.role_seeds) : "");
   {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->roles.find(key);
@@ -520,7 +522,18 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     if (buf.size() == 64) perm.assign(buf.begin(), buf.end());
   } else {
     const int threads = g_worker ? 1 : (int)std::max(1u, std::thread::hardware_concurrency());
-    perm = bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull, threads);
+    // role_seeds independent searches (different generator seeds), the
+    // permutation of least modelled cost wins (ties: the first seed)
+    double best = 0;
+    for (int r = 0; r < std::max(1, p->opt.role_seeds); r++) {
+      std::vector<int8_t> pm =
+          bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull + 0x9e3779b9ull * r, threads);
+      if (p->opt.role_seeds <= 1) { perm = pm; break; }
+      bfa::KernelSpec sp = *spec;
+      sp.perm = pm;
+      const double c = bfa::model_cost(p->parsed, sp);
+      if (r == 0 || c < best) { best = c; perm = pm; }
+    }
     if (!p->opt.jit_cache) {
     } else if (perm.empty()) {
       char z = 0;
@@ -1081,7 +1094,7 @@ std::string options_key(const Options& o) {
   std::ostringstream k;
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
-    << ',' << o.role_budget << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
+    << ',' << o.role_budget << ',' << o.role_seeds << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
     << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level << ',' << o.queue_slot_bits;
   return k.str();
 }
@@ -2255,6 +2268,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
   else if (k == "role_search") { if (v < 0 || v > 1) return bad(); p->opt.role_search = (int)v; }
   else if (k == "role_budget") { if (v < 1 || v > 4096) return bad(); p->opt.role_budget = (int)v; }
+  else if (k == "role_seeds") { if (v < 1 || v > 64) return bad(); p->opt.role_seeds = (int)v; }
   else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }
   else if (k == "segment_remat") { if (v < 0 || v > 64) return bad(); p->opt.segment_remat = (int)v; }
   else if (k == "kernel_cofactor_bits") { if (v < 0 || v > 8) return bad(); p->opt.kernel_cofactor_bits = (int)v; }

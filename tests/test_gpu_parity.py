@@ -481,7 +481,7 @@ def test_decomposed_large_modules_vs_oracle():
 
 def test_decomposed_bench_preset_full_cube():
     """The bench's replay configuration itself (presets.DECOMPOSED: 32768
-    Shannon leaves in work-queue modules of <= 512 bodies) over the whole C5
+    Shannon leaves in work-queue modules of <= 256 bodies) over the whole C5
     cube equals the oracle-checked exhaustive kernel's count, replay after
     replay, and f + ~f covers the cube on the exhaustive side (P-11)."""
     text, n, _ = W.config("c5")
