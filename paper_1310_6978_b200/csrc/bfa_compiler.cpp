@@ -512,7 +512,8 @@ static inline uint8_t unary_code(int v0, int v1) {
 }
 
 MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
-                   const std::vector<uint8_t>& var_level, const double weights[4], double imad_cost) {
+                   const std::vector<uint8_t>& var_level, const double weights[4], double imad_cost,
+                   int area_passes) {
   const size_t N = dag.nodes.size();
   MapResult res;
   res.node_level.assign(N, 0);
@@ -626,6 +627,66 @@ MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
     std::copy(cand, cand + nc, cuts_of(n));
     cuts_of(n)[nc] = triv;
     ncut[n] = (uint8_t)(nc + 1);
+  }
+  // exact-area recovery (the priority-cut mapper's final passes): with the
+  // cover's reference counts, every referenced gate re-chooses among its
+  // cuts (and its IMAD cell) the one that adds the least loop-weighted area
+  // given everything else in the cover -- area flow only estimates sharing
+  if (area_passes > 0) {
+    std::vector<int> choice(N, 0);   // cut index, or -1 = IMAD cell
+    for (size_t n = 0; n < N; n++) choice[n] = use_imad[n] ? -1 : 0;
+    std::vector<uint32_t> refs(N, 0);
+    auto is_gate = [&](uint32_t l) { return dag.nodes[l].kind == NK_GATE; };
+    auto cell_w = [&](uint32_t n, int ch) {
+      return weights[res.node_level[n]] * (ch < 0 ? imad_cost : 1.0);
+    };
+    auto leaves = [&](uint32_t n, int ch, uint32_t* L) -> int {
+      if (ch < 0) { L[0] = imad[n].x; L[1] = imad[n].u; return 2; }
+      const Cut& c = cuts_of(n)[ch];
+      for (int q = 0; q < c.n; q++) L[q] = c.leaf[q];
+      return c.n;
+    };
+    std::function<double(uint32_t, int)> ref = [&](uint32_t n, int ch) {
+      double a = cell_w(n, ch);
+      uint32_t L[3];
+      const int k = leaves(n, ch, L);
+      for (int q = 0; q < k; q++)
+        if (is_gate(L[q]) && refs[L[q]]++ == 0) a += ref(L[q], choice[L[q]]);
+      return a;
+    };
+    std::function<double(uint32_t, int)> deref = [&](uint32_t n, int ch) {
+      double a = cell_w(n, ch);
+      uint32_t L[3];
+      const int k = leaves(n, ch, L);
+      for (int q = 0; q < k; q++)
+        if (is_gate(L[q]) && --refs[L[q]] == 0) a += deref(L[q], choice[L[q]]);
+      return a;
+    };
+    for (Lit o : outputs) {
+      const uint32_t r = lit_node(o);
+      if (is_gate(r) && refs[r]++ == 0) ref(r, choice[r]);
+    }
+    for (int pass = 0; pass < area_passes; pass++) {
+      for (size_t n = 0; n < N; n++) {
+        if (!refs[n] || !is_gate((uint32_t)n)) continue;
+        deref((uint32_t)n, choice[n]);
+        int best = choice[n];
+        double best_a = 1e300;
+        const int nc = (int)ncut[n] - 1;  // the trivial cut last
+        for (int ch = (imad[n].ok ? -1 : 0); ch < nc; ch++) {
+          const double a = ref((uint32_t)n, ch);
+          deref((uint32_t)n, ch);
+          if (a < best_a - 1e-9 || (a <= best_a + 1e-9 && ch == choice[n])) { best_a = a; best = ch; }
+        }
+        choice[n] = best;
+        ref((uint32_t)n, best);
+      }
+    }
+    for (size_t n = 0; n < N; n++) {
+      if (!is_gate((uint32_t)n) || !in_cone[n]) continue;
+      use_imad[n] = choice[n] < 0;
+      if (choice[n] > 0) std::swap(cuts_of(n)[0], cuts_of(n)[choice[n]]);
+    }
   }
   // cover extraction from the outputs (reverse topological order)
   std::vector<uint8_t> req(N, 0);
@@ -902,7 +963,7 @@ static MapResult choose_mapping(const Built& b, const KernelSpec& spec, double* 
     else sweep = {0.0, 0.6, 0.75, 0.9, 1.0, 1.15, 1.3, 1.6, 2.0, 3.0};
   }
   for (double c : sweep) {
-    MapResult r = map_luts(b.D, b.outs, b.var_level, b.w, c);
+    MapResult r = map_luts(b.D, b.outs, b.var_level, b.w, c, spec.area_passes);
     double tm = model_time(b, r, spec);
     if (tm < best - 1e-9) { best = tm; mr = std::move(r); cost = c; }
   }
@@ -945,10 +1006,12 @@ static void dfs_order(MapResult* mr, const std::vector<Lit>& outs) {
 }
 
 double model_cost(const Parsed& prog, const KernelSpec& spec) {
+  KernelSpec sp = spec;
+  sp.area_passes = 0;  // the search compares area-flow covers; emission refines the winner
   Built b;
-  build_specialised(prog, spec, &b);
+  build_specialised(prog, sp, &b);
   double t = 0;
-  choose_mapping(b, spec, &t, nullptr);
+  choose_mapping(b, sp, &t, nullptr);
   return t;
 }
 

@@ -115,9 +115,10 @@ struct MapResult {
 };
 // imad_cost > 0 enables IMAD cells for gates with a word-uniform input, at
 // that cost relative to one LUT (two-resource area flow).
+// area_passes > 0: that many exact-area recovery passes after area flow.
 MapResult map_luts(const Dag& dag, const std::vector<Lit>& outputs,
                    const std::vector<uint8_t>& var_level, const double weights[4],
-                   double imad_cost = 0.0);
+                   double imad_cost = 0.0, int area_passes = 0);
 
 // ---------------------------------------------------------------- kernels
 enum KernelMode : int { KM_COUNT = 0, KM_EVAL = 1 };
@@ -138,6 +139,8 @@ struct KernelSpec {
                               // word/valuation index (empty = identity)
   std::string body_name;      // non-empty: emit the specialised kernel as a
                               // __device__ __noinline__ body of a multi-body kernel
+  int area_passes = 1;        // exact-area recovery passes of the LUT mapper (emission;
+                              // model_cost -- the role search's objective -- uses 0)
   int count_shift = 0;        // count mode: the count is scaled by 2^count_shift
                               // (support reduction: variables outside the support)
 };
