@@ -419,15 +419,15 @@ __global__ void __launch_bounds__(kCompactThreads) tile_write_kernel(const u64* 
 // assumed) program is deposited on the original letter ids (killed letters
 // reinstated from fixed_values), then written as n_all characters '0'/'1',
 // the paper's b_1 (id n_all - 1) first, and '\n'.
-__constant__ int c_free_ids[64];
+struct FreeIds { int id[64]; };  // by value in the parameter bank: no global state between calls
 
 __global__ void __launch_bounds__(256) rows_kernel(const u64* __restrict__ mu, u64 count, int n_free, int n_all,
-                                                   u64 fixed_values, char* __restrict__ rows) {
+                                                   u64 fixed_values, char* __restrict__ rows, const FreeIds ids) {
   const u64 stride = (u64)gridDim.x * blockDim.x;
   for (u64 r = (u64)blockIdx.x * blockDim.x + threadIdx.x; r < count; r += stride) {
     const u64 m = mu[r];
     u64 full = fixed_values;
-    for (int k = 0; k < n_free; k++) full |= ((m >> k) & 1ull) << c_free_ids[k];
+    for (int k = 0; k < n_free; k++) full |= ((m >> k) & 1ull) << ids.id[k];
     char* row = rows + r * (u64)(n_all + 1);
     for (int j = 0; j < n_all; j++) row[j] = (char)('0' + ((full >> (n_all - 1 - j)) & 1ull));
     row[n_all] = '\n';
@@ -461,11 +461,11 @@ cudaError_t compact_models(const uint64_t* vec, uint64_t n_words, uint64_t lo, u
 
 cudaError_t rows(const uint64_t* mu, uint64_t count, int n_free, const int* free_ids, int n_all,
                  uint64_t fixed_values, char* out, cudaStream_t st) {
-  cudaError_t e = cudaMemcpyToSymbolAsync(c_free_ids, free_ids, sizeof(int) * n_free, 0, cudaMemcpyHostToDevice, st);
-  if (e != cudaSuccess) return e;
   if (!count) return cudaSuccess;
+  FreeIds ids{};
+  for (int k = 0; k < n_free && k < 64; k++) ids.id[k] = free_ids[k];
   const unsigned grid = (unsigned)std::min<u64>((count + 255) / 256, 148ull * 8);
-  rows_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const u64*>(mu), count, n_free, n_all, fixed_values, out);
+  rows_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const u64*>(mu), count, n_free, n_all, fixed_values, out, ids);
   return cudaGetLastError();
 }
 
