@@ -67,6 +67,11 @@ def parse_args():
     ap.add_argument("--no-extras", action="store_true", help="skip the replay and the extra config lines")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend (gloo + --share-device: functional multi-rank runs on one GPU)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="every rank on cuda:0 (functional test of the N > 1 path on a one-GPU box; not a "
+                         "scaling measurement)")
     ap.add_argument("--options", default=None,
                     help="JSON dict of program options applied on top of the preset (profiling variants)")
     return ap.parse_args()
@@ -317,10 +322,14 @@ def run_bfa(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    gpu = 0 if args.share_device else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     text, n, expect = W.config(args.config)
     extra_opts = json.loads(args.options) if args.options else {}
@@ -351,7 +360,7 @@ def run_bfa(args):
     launch = bfa.last_launch()
 
     timer = Timer(torch, stream, dev)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -426,7 +435,10 @@ def run_bfa(args):
         "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u32 (bitwise LOP3/IMAD on 32-valuation words)",
         "data": "synthetic (seeded generator, workloads/__init__.py)",
-        "config": config_block(args.config, n, world),
+        "config": dict(config_block(args.config, n, world),
+                       **({"functional_multi_rank": f"{world} ranks sharing cuda:0 over {args.backend}: checks the "
+                                                    "N > 1 path, not a scaling measurement"}
+                          if args.share_device and world > 1 else {})),
         "program": {"gates_G": info["gates"], "luts_L": info["luts"], "support": info["support"],
                     "options": dict(preset, **extra_opts)},
         "count": final, "count_expected": expect, "count_verified": verified,

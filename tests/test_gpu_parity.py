@@ -780,3 +780,31 @@ def test_programs_release_device_memory():
     churn(200)
     free1 = torch.cuda.mem_get_info()[0]
     assert free0 - free1 < 64 << 20, (free0 - free1) >> 20
+
+
+def test_bench_multi_rank_functional():
+    """The bench's N > 1 path end to end on the one GPU this pool gives:
+    torchrun with 2 ranks sharing cuda:0 over gloo (a functional run, not a
+    scaling measurement): rank-0-first preparation, per-rank cofactor ranges
+    with the same kernel, the count all-reduce, max-over-ranks timing and the
+    cold e2e -- the reported count is the closed form."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", str(port), os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "2",
+           "--warmup", "3", "--e2e-steps", "1", "--no-extras", "--no-cpu-baseline", "--config", "c4",
+           "--backend", "gloo", "--share-device"]
+    p = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [x for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["count"] == 130023 and d["value"] > 0 and d["e2e"]["value"] > 0
