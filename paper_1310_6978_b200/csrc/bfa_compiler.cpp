@@ -949,7 +949,44 @@ static double model_time(const Built& b, const MapResult& r, const KernelSpec& s
     i = j;
   }
   const double other = spec.generic ? 4.0 : b.S + b.S / 2.0 + 2.0 + 2.0 * b.m;
-  return std::max({2 * (A + other), 2 * F, A + F + other});
+  double t = std::max({2 * (A + other), 2 * F, A + F + other});
+  // register pressure: every thread- / outer-level value an inner cell reads
+  // (and every derived IMAD operand of one) stays live across the inner
+  // loop; past the register file the kernel spills (C5 at slot 7: 255
+  // registers + 150-400 B of spill stores, 1.6x slower with 227 live-in
+  // values; slot 5, 177 live-in values: no spill).  Each live value beyond
+  // the budget costs 1 % of the iteration.
+  if (!spec.generic && b.m > 0) {
+    std::vector<uint64_t> live;   // hoisted nodes, and hoisted IMAD operand registers (u, k, c)
+    for (const Lut& L : r.luts) {
+      if (L.level != 3) continue;
+      if (L.kind == 1 && b.D.nodes[L.in[0]].kind != NK_CONST) {
+        const uint32_t u = L.in[1];
+        if (r.node_level[u] < 3) {
+          int m0, c0, m1, c1;
+          Emitter::mc(L.f0, &m0, &c0);
+          Emitter::mc(L.f1, &m1, &c1);
+          for (auto kc : {std::make_pair(m0 - m1, m0), std::make_pair(c0 - c1, c0)})
+            if (kc.first != 0 && !(kc.first == 1 && kc.second == 0))
+              live.push_back(1ull << 63 | (uint64_t)u << 16 | (uint64_t)(kc.first + 8) << 8 | (uint64_t)(kc.second + 8));
+            else if (kc.first == 1)
+              live.push_back(u);
+        }
+        if (r.node_level[L.in[0]] < 3) live.push_back(L.in[0]);
+        continue;
+      }
+      for (int q = 0; q < L.nin; q++) {
+        const uint32_t x = L.in[q];
+        if (b.D.nodes[x].kind != NK_CONST && r.node_level[x] < 3) live.push_back(x);
+      }
+    }
+    std::sort(live.begin(), live.end());
+    live.erase(std::unique(live.begin(), live.end()), live.end());
+    const double budget = 180.0;  // of 255, leaving ~75 for the inner loop's own temporaries
+    const double excess = (double)live.size() - budget;
+    if (excess > 0) t *= 1.0 + 0.01 * excess;
+  }
+  return t;
 }
 
 // Technology mapping.  With dual_pipe, gates that have a word-uniform input
@@ -1481,6 +1518,35 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
     if (lv == 3) st.derived_inner += (uint32_t)kv.second.size();
     if (lv == 2) st.derived_outer += (uint32_t)kv.second.size();
   }
+  auto level_of = [&](int v) { return (int)b.var_level[v]; };
+  // The count of one thread-iteration is sum over the 2^s slot outputs of
+  // popc(output).  Per distinct output node x with k positive and j
+  // complemented uses that is (k - j) popc(x) + 32 j.  Outputs computed at the
+  // thread / outer level are counted once per outer iteration (x 2^m); inner
+  // outputs right after the cell that defines them, so no slot output stays
+  // live to the end of the body (register pressure).
+  struct OutUse { int k = 0, j = 0; };
+  std::map<uint32_t, OutUse> out_use;
+  uint32_t const_pop = 0;
+  for (int sl = 0; sl < S; sl++) {
+    const Lit o = outs[sl];
+    const Node& on = D.nodes[lit_node(o)];
+    if (on.kind == NK_CONST) { const_pop += (uint32_t)__builtin_popcount(lit_neg(o) ? ~on.val : on.val); continue; }
+    OutUse& u = out_use[lit_node(o)];
+    (lit_neg(o) ? u.j : u.k)++;
+  }
+  auto node_level = [&](uint32_t x) {
+    return D.nodes[x].kind == NK_VAR ? level_of((int)D.nodes[x].val) : (int)mr.node_level[x];
+  };
+  uint32_t inner_const = 0, outer_const = const_pop;
+  auto count_out = [&](uint32_t x, const char* acc) {  // acc += (k - j) popc(x); constants aside
+    const OutUse& u = out_use.at(x);
+    (node_level(x) == 3 ? inner_const : outer_const) += 32u * (uint32_t)u.j;
+    if (u.k == u.j) return;
+    body << "\tpopc.b32 %t2, " << E.reg(x) << ";\n";
+    if (u.k - u.j == 1) body << "\tadd.u32 " << acc << ", " << acc << ", %t2;\n";
+    else body << "\tmad.lo.u32 " << acc << ", %t2, " << ptx_imm((uint32_t)(u.k - u.j)) << ", " << acc << ";\n";
+  };
   auto emit_level = [&](int lvl) {
     for (const Lut& L : mr.luts) {
       if (L.level != lvl) continue;
@@ -1488,9 +1554,9 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
       uint32_t* luts = lvl == 1 ? &st.luts_thread : lvl == 2 ? &st.luts_outer : &st.luts_inner;
       uint32_t* imads = lvl == 1 ? &st.imads_thread : lvl == 2 ? &st.imads_outer : &st.imads_inner;
       (*(L.kind == 1 ? imads : luts))++;
+      if (lvl == 3 && out_use.count(L.root)) count_out(L.root, "%a32");
     }
   };
-  auto level_of = [&](int v) { return (int)b.var_level[v]; };
   const int unit = s + t + m;
   // ---- prologue: chunk bounds and thread-level variables/cells
   body << "\tmov.u32 %tidr, %tid.x;\n";
@@ -1526,6 +1592,10 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
       st.outer_vars++;
     }
   emit_level(2);
+  // thread- and outer-level outputs: counted once per outer iteration
+  body << "\tmov.u32 %po, 0;\n";
+  for (auto& ou : out_use)
+    if (node_level(ou.first) < 3) count_out(ou.first, "%po");
   body << "\tmov.u32 %a32, 0;\n\tmov.u32 %ii, 0;\n"
        << "$L_inner:\n\t.pragma \"nounroll\";\n";
   for (int v = 0; v < 64; v++)
@@ -1533,23 +1603,14 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
       const int k = b.pos[v] - 5 - s - t;
       body << "\tshl.b32 %t0, %ii, " << (31 - k) << ";\n\tshr.s32 %v" << v << ", %t0, 31;\n";
       E.emit_derived(var_node[v]);
+      if (out_use.count(var_node[v])) count_out(var_node[v], "%a32");
       st.inner_vars++;
     }
   emit_level(3);
-  uint32_t const_pop = 0;
-  for (int sl = 0; sl < S; sl++) {
-    const Lit o = outs[sl];
-    const Node& on = D.nodes[lit_node(o)];
-    if (on.kind == NK_CONST) {
-      const_pop += (uint32_t)__builtin_popcount(lit_neg(o) ? ~on.val : on.val);
-      continue;
-    }
-    if (lit_neg(o)) body << "\tnot.b32 %t1, " << E.reg(lit_node(o)) << ";\n\tpopc.b32 %t2, %t1;\n";
-    else body << "\tpopc.b32 %t2, " << E.reg(lit_node(o)) << ";\n";
-    body << "\tadd.u32 %a32, %a32, %t2;\n";
-  }
-  if (const_pop) body << "\tadd.u32 %a32, %a32, " << const_pop << ";\n";
-  body << "\tadd.u32 %ii, %ii, 1;\n\tsetp.lt.u32 %p1, %ii, " << (1u << m) << ";\n\t@%p1 bra $L_inner;\n"
+  if (inner_const) body << "\tadd.u32 %a32, %a32, " << inner_const << ";\n";
+  body << "\tadd.u32 %ii, %ii, 1;\n\tsetp.lt.u32 %p1, %ii, " << (1u << m) << ";\n\t@%p1 bra $L_inner;\n";
+  if (outer_const) body << "\tadd.u32 %po, %po, " << outer_const << ";\n";
+  body << "\tshl.b32 %po, %po, " << m << ";\n\tadd.u32 %a32, %a32, %po;\n"
        << "\tcvt.u64.u32 %x64, %a32;\n\tadd.u64 %acc, %acc, %x64;\n"
        << "\tadd.u64 %o, %o, 1;\n\tsetp.lt.u64 %p0, %o, %oe;\n\t@%p0 bra $L_outer;\n"
        << "$L_done:\n";
@@ -1585,7 +1646,7 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
           ".param .u64 p_count)\n" << bounds << "{\n";
   }
   os << "\t.reg .pred %p<2>;\n\t.reg .b32 %t<3>, %c<" << D.nodes.size() << ">, %v<64>;\n"
-     << "\t.reg .b32 %tidr, %bid, %nb, %ii, %a32, %lo, %hi, %lo2, %hi2;\n"
+     << "\t.reg .b32 %tidr, %bid, %nb, %ii, %a32, %po, %lo, %hi, %lo2, %hi2;\n"
      << "\t.reg .b64 %A, %O, %cnt, %b, %q, %rr, %ob, %oe, %o, %wo, %acc, %x64, %y64;\n";
   for (auto& kv : E.derived)
     for (auto& kc : kv.second) os << "\t.reg .b32 " << PtxEmitter::dname(kv.first, kc.first, kc.second) << ";\n";

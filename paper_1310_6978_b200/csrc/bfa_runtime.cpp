@@ -325,7 +325,9 @@ const char* ptx_opt(const std::string& src) {
   return "-O3";
 }
 
-int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
+// spill_bytes (nullable) receives the bytes of register spill stores ptxas
+// reports for the module (its -v info log), -1 if unknown
+int ptx_compile(const std::string& ptx, std::vector<char>* cubin, int* spill_bytes = nullptr) {
   if (const char* dir = getenv("BFA_DUMP_SRC")) {  // debugging: keep every generated source
     char path[4096];
     snprintf(path, sizeof path, "%s/%016llx.ptx", dir, (unsigned long long)fnv64(ptx.data(), ptx.size()));
@@ -334,8 +336,8 @@ int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
   nvPTXCompilerHandle h = nullptr;
   nvPTXCompileResult r = nvPTXCompilerCreate(&h, ptx.size(), ptx.c_str());
   if (r != NVPTXCOMPILE_SUCCESS) return set_err(BFA_E_JIT, "nvPTXCompilerCreate: %d", (int)r);
-  const char* opts[] = {kPtxOpts[0], ptx_opt(ptx)};
-  r = nvPTXCompilerCompile(h, 2, opts);
+  const char* opts[] = {kPtxOpts[0], ptx_opt(ptx), "-v"};
+  r = nvPTXCompilerCompile(h, 3, opts);
   if (r != NVPTXCOMPILE_SUCCESS) {
     size_t n = 0;
     nvPTXCompilerGetErrorLogSize(h, &n);
@@ -349,6 +351,20 @@ int ptx_compile(const std::string& ptx, std::vector<char>* cubin) {
   nvPTXCompilerGetCompiledProgramSize(h, &sz);
   cubin->resize(sz);
   nvPTXCompilerGetCompiledProgram(h, cubin->data());
+  if (spill_bytes) {  // "... N bytes spill stores, M bytes spill loads" per function
+    size_t n = 0;
+    nvPTXCompilerGetInfoLogSize(h, &n);
+    std::string log(n, '\0');
+    if (n) nvPTXCompilerGetInfoLog(h, &log[0]);
+    int total = 0;
+    for (size_t at = log.find(" bytes spill stores"); at != std::string::npos;
+         at = log.find(" bytes spill stores", at + 1)) {
+      size_t b = at;
+      while (b > 0 && isdigit((unsigned char)log[b - 1])) b--;
+      total += atoi(log.c_str() + b);
+    }
+    *spill_bytes = log.empty() ? -1 : total;
+  }
   nvPTXCompilerDestroy(&h);
   return BFA_OK;
 }
@@ -364,13 +380,26 @@ std::string ptx_cache_key(const std::string& src) {
   return h.hex();
 }
 
-int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin, bool use_cache = true) {
+// spill (nullable): bytes of register spill stores of a PTX module (kept
+// beside the cubin in the persistent cache), -1 if unknown
+int nvrtc_compile_cached(const std::string& src, std::vector<char>* cubin, bool use_cache = true, int* spill = nullptr) {
   const bool ptx = is_ptx_source(src);
-  if (!use_cache) return ptx ? ptx_compile(src, cubin) : nvrtc_compile(src, cubin);
-  const std::string name = "k_" + (ptx ? ptx_cache_key(src) : cubin_cache_key(src)) + ".cubin";
-  if (cache_read(name, cubin)) return BFA_OK;
-  int rc = ptx ? ptx_compile(src, cubin) : nvrtc_compile(src, cubin);
-  if (rc == BFA_OK) cache_write(name, cubin->data(), cubin->size());
+  if (spill) *spill = -1;
+  if (!use_cache) return ptx ? ptx_compile(src, cubin, spill) : nvrtc_compile(src, cubin);
+  const std::string key = "k_" + (ptx ? ptx_cache_key(src) : cubin_cache_key(src));
+  if (cache_read(key + ".cubin", cubin)) {
+    std::vector<char> info;
+    if (spill && cache_read(key + ".spill", &info)) *spill = atoi(std::string(info.begin(), info.end()).c_str());
+    return BFA_OK;
+  }
+  int rc = ptx ? ptx_compile(src, cubin, spill) : nvrtc_compile(src, cubin);
+  if (rc == BFA_OK) {
+    if (spill && *spill >= 0) {
+      const std::string t = std::to_string(*spill);
+      cache_write(key + ".spill", t.data(), t.size());
+    }
+    cache_write(key + ".cubin", cubin->data(), cubin->size());
+  }
   return rc;
 }
 
@@ -421,6 +450,7 @@ struct JitEntry {
   std::map<int, CUmodule> mod;    // per device (unloaded with the entry)
   std::map<int, int> occupancy;   // blocks per SM per device
   int regs = 0;
+  int spill = -1;                 // register spill-store bytes (PTX modules; -1 unknown)
   ~JitEntry() {
     for (auto& m : mod)
       if (m.second && drv().ModuleUnload) drv().ModuleUnload(m.second);
@@ -496,6 +526,10 @@ std::string spec_key(const bfa::KernelSpec& s) {
 // Count mode over an aligned sub-cube of 2^k_free valuations: search (once per
 // program and variant) the variable->position permutation whose cover is
 // cheapest; the kernel then enumerates the same sub-cube in permuted order.
+struct JitEntry;
+int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntry** out, CUfunction* fn);
+bool use_ptx(const bfa_prog* p, const bfa::KernelSpec& spec);
+
 void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
   bfa_prog* p = const_cast<bfa_prog*>(cp);
   spec->perm.clear();
@@ -509,7 +543,7 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
   }
   // persistent cache: hash of the DAG reachable from the root + the variant
   bfa::Sha256 h;
-  h.update("bfa-roles-v2|").update(key).update("|");
+  h.update("bfa-roles-v3|search-20261019b|").update(key).update("|");
   for (const bfa::Node& nd : p->parsed.dag.nodes) {
     uint32_t rec[4] = {(uint32_t)nd.kind | ((uint32_t)nd.tt << 8), nd.a, nd.b, nd.val};
     h.update(rec, sizeof rec);
@@ -522,18 +556,30 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     if (buf.size() == 64) perm.assign(buf.begin(), buf.end());
   } else {
     const int threads = g_worker ? 1 : (int)std::max(1u, std::thread::hardware_concurrency());
-    // role_seeds independent searches (different generator seeds), the
-    // permutation of least modelled cost wins (ties: the first seed)
-    double best = 0;
+    // role_seeds independent searches (different generator seeds), in order
+    // of modelled cost; the first whose compiled kernel spills no registers
+    // wins (the model counts cells, not registers: at slot 7 a cheaper cover
+    // can spill and run 1.6x slower), else the cheapest
+    std::vector<std::pair<double, std::vector<int8_t>>> cand;
     for (int r = 0; r < std::max(1, p->opt.role_seeds); r++) {
       std::vector<int8_t> pm =
           bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull + 0x9e3779b9ull * r, threads);
-      if (p->opt.role_seeds <= 1) { perm = pm; break; }
+      if (p->opt.role_seeds <= 1) { cand.push_back({0.0, pm}); break; }
       bfa::KernelSpec sp = *spec;
       sp.perm = pm;
-      const double c = bfa::model_cost(p->parsed, sp);
-      if (r == 0 || c < best) { best = c; perm = pm; }
+      cand.push_back({bfa::model_cost(p->parsed, sp), pm});
     }
+    std::stable_sort(cand.begin(), cand.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    perm = cand[0].second;
+    if (cand.size() > 1 && use_ptx(p, *spec))
+      for (auto& c : cand) {
+        bfa::KernelSpec sp = *spec;
+        sp.perm = c.second.empty() ? std::vector<int8_t>{} : c.second;
+        JitEntry* e = nullptr;
+        const int rc2 = get_kernel(p, sp, -1, &e, nullptr);
+        if (getenv("BFA_DEBUG_ROLES")) fprintf(stderr, "role candidate cost %.1f rc %d spill %d\n", c.first, rc2, e ? e->spill : -9);
+        if (rc2 == BFA_OK && e && e->spill == 0) { perm = c.second; break; }
+      }
     if (!p->opt.jit_cache) {
     } else if (perm.empty()) {
       char z = 0;
@@ -576,7 +622,7 @@ int get_kernel(const bfa_prog* cp, const bfa::KernelSpec& spec, int dev, JitEntr
   if (!e) {
     auto ne = std::make_unique<JitEntry>();
     ne->source = ptx ? bfa::emit_ptx(p->parsed, spec, &ne->stats) : bfa::emit_kernel(p->parsed, spec, &ne->stats);
-    int rc = nvrtc_compile_cached(ne->source, &ne->cubin, p->opt.jit_cache);
+    int rc = nvrtc_compile_cached(ne->source, &ne->cubin, p->opt.jit_cache, &ne->spill);
     if (rc) return rc;
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->jit.find(key);
