@@ -68,7 +68,7 @@ extern "C" {
 #define BFA_E_ARG    -2   /* NULL pointer, misaligned range, bad option          */
 #define BFA_E_RANGE  -3   /* n > 63, n <= max variable id, range outside [0,2^n) */
 #define BFA_E_CUDA   -4   /* CUDA runtime/driver failure or no device            */
-#define BFA_E_JIT    -5   /* NVRTC / module load failure                         */
+#define BFA_E_JIT    -5   /* JIT (PTX compiler / NVRTC) or module load failure   */
 #define BFA_E_NOMEM  -6
 
 typedef struct bfa_prog bfa_prog;
@@ -216,7 +216,7 @@ int bfa_count_range(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi,
 int bfa_roles(const bfa_prog* p, int n, int k_free, int sms, int8_t* perm_out);
 
 /* Host-only preparation of the count kernel for aligned 2^k_free sub-cubes
- * (e.g. one rank's cofactor range, k_free = n - log2 P): role search + NVRTC,
+ * (e.g. one rank's cofactor range, k_free = n - log2 P): role search + JIT,
  * results cached in p and in the persistent JIT cache, so other processes
  * (the other ranks) load them instead of re-deriving them.  No device needed
  * (sms <= 0: the current device's, else 148).  BFA_E_ARG when such a count
@@ -262,7 +262,7 @@ int64_t bfa_shard_piece_text(const bfa_prog* p, int n, int world, int index, cha
 
 /* Host-only preparation (SURVEY.md §8(b) bfa_compile's JIT, ahead of time):
  * everything bfa_count(p, n) compiles before its first launch -- the
- * decomposition, role searches, kernel emission and NVRTC -- for a device
+ * decomposition, role searches, kernel emission and JIT compile -- for a device
  * with `sms` SMs (<= 0: the current device's, else 148).  Needs no GPU and
  * launches nothing; results are cached in p (and in the persistent JIT cache).
  * Returns BFA_OK, BFA_E_RANGE (bad n) or BFA_E_JIT. */
