@@ -455,6 +455,25 @@ def test_count_shard_sums_to_count():
         assert a + b == 1 << n, world
 
 
+def test_decomposed_body_options_vs_oracle():
+    """Work-queue body variants (more slot bits, one inner bit, the light
+    tail's smaller bodies, ptxas -O1) on a 2^24 C5 sub-cube vs the oracle."""
+    text, n, _ = W.config("c5")
+    base = bfa.Program(text)
+    rng = np.random.default_rng(99)
+    while True:
+        lo = int(rng.integers(0, 1 << (n - 24))) << 24
+        q, _, _ = base.assume(n, {v: (lo >> v) & 1 for v in range(24, n)})
+        if q.info["const_value"] == -1 and q.info["gates"] >= 150:
+            break
+    expect = oracle.count(text, n, lo, lo + (1 << 24))
+    for extra in ({"queue_slot_bits": 6, "queue_inner": 1}, {"queue_light_pct": 40, "queue_opt_level": 1}):
+        p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=64, decompose_min_k=24,
+                          split_min_vars=19, **extra)
+        assert int(p.count_range(n, lo, lo + (1 << 24)).item()) == expect, extra
+        assert bfa.last_launch()["queue"]["bodies"] > 1
+
+
 def test_decomposed_large_modules_vs_oracle():
     """Work-queue modules of up to 512 bodies each (the bench preset's module
     size) on an oracle-checkable sub-cube: a 2^26 C5 sub-cube decomposed into
