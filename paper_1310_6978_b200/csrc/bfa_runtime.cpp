@@ -1796,6 +1796,7 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     // preparation: work-queue bodies search longer (C5, 32768 leaves: budget
     // 200 -> 1.31 ms, 400 -> 1.20 ms)
     const_cast<bfa_prog*>(src)->opt.role_budget = light[e] ? std::max(16, o.queue_role_budget / 4) : o.queue_role_budget;
+    const_cast<bfa_prog*>(src)->opt.role_seeds = 1;  // one search per body (no per-candidate compiles)
     resolve_roles(src, &spec, b.nv);
     b.name = "bfa_body_" + std::to_string(i);
     spec.body_name = "bfa_body_X";  // placeholder: identical bodies of a module share one copy
