@@ -1752,7 +1752,23 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
       light[x.second] = 1;
     }
   }
+  // identical leaves (the same reduced program over the same variables --
+  // different branches of the split tree can reduce to the same cofactor)
+  // are searched and emitted once
+  std::vector<size_t> rep(elig.size());
+  {
+    std::vector<std::string> fp(elig.size());
+    parallel_for(elig.size(), [&](size_t e) {
+      const bfa_prog* q = kids[elig[e]].get();
+      fp[e] = o.queue_support ? std::to_string(e)
+                              : bfa::sha256_hex(std::to_string(q->piece_nv) + "|" + std::to_string(light[e]) + "|" +
+                                                bfa::to_text(q->parsed));
+    });
+    std::unordered_map<std::string, size_t> first;
+    for (size_t e = 0; e < elig.size(); e++) rep[e] = first.emplace(fp[e], e).first->second;
+  }
   parallel_for(elig.size(), [&](size_t e) {
+    if (rep[e] != e) return;  // filled from its representative below
     const size_t i = elig[e];
     bfa_prog* q = kids[i].get();
     Body& b = B[e];
@@ -1809,6 +1825,18 @@ int ensure_queue(bfa_prog* holder, const std::string& key, std::vector<std::uniq
     b.cost_o = std::ldexp(inner + 2.0 * (1 << b.s) + 6.0, b.m) + outer + 12.0;
     b.cost = (double)b.O * b.cost_o;
   });
+  for (size_t e = 0; e < elig.size(); e++) {
+    if (rep[e] == e) continue;
+    const Body& r = B[rep[e]];
+    Body& b = B[e];
+    b.name = "bfa_body_" + std::to_string(elig[e]);
+    b.src = r.src;
+    b.st = r.st;
+    b.O = r.O;
+    b.m = r.m; b.nv = r.nv; b.s = r.s; b.shift = r.shift;
+    b.cost = r.cost; b.size = r.size; b.cost_o = r.cost_o;
+    b.hash = r.hash;
+  }
   bfa_prog::Queue Q;
   Q.queued.assign(kids.size(), 0);
   Q.bodies = elig.size();
