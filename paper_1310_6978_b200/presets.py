@@ -10,10 +10,10 @@ timed region (2^slot_bits slot cofactors constant-folded into the
 straight-line body, variable roles searched, LOP3 + IMAD cells).  Nothing is
 decided at preparation time.  Chosen by full-cube sweeps on a B200
 (profiles/r02/sweep_exhaustive.jsonl):
-  C5 (n=42): slot 7, inner 2, role budget 400 -> 154 ms per 2^42
-             (slot 6 / inner 3: 170 ms; slot 5 / inner 4 / budget 200: 229 ms;
-             slot 8: 292-509 ms, i-cache and spills); 3 role-search seeds:
-             24.8 -> 23.6 cells per word
+  C5 (n=42): slot 7, inner 2, role budget 800, 3 seeds with the spill check
+             -> 144.5 ms per 2^42 (budget 400: 149 ms; one seed: spills, 223 ms;
+             slot 6 / inner 3: 170 ms; slot 5 / inner 4 / budget 200: 229 ms;
+             slot 8: 292-509 ms, i-cache and spills)
   C4 (n=36): slot 8, inner 2 -> 0.079 ms per 2^36 (slot 5 / inner 4: 0.296 ms)
 
 cold(cfg): the plan of least preparation + ONE count (what a single cold
@@ -30,7 +30,7 @@ its preparation cost.
 """
 
 EXHAUSTIVE = {"slot_bits": 7, "thread_bits": 8, "inner_bits": 2, "dual_pipe": 1, "imad_cost_pct": 50,
-              "min_blocks": 0, "role_budget": 400, "role_seeds": 3, "kernel_cofactor_bits": 0, "split_pieces": 0}
+              "min_blocks": 0, "role_budget": 800, "role_seeds": 3, "kernel_cofactor_bits": 0, "split_pieces": 0}
 
 _EXHAUSTIVE_BY_CONFIG = {
     "c4": dict(EXHAUSTIVE, slot_bits=8, inner_bits=2, role_budget=200, role_seeds=1),
