@@ -576,9 +576,7 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
         bfa::KernelSpec sp = *spec;
         sp.perm = c.second.empty() ? std::vector<int8_t>{} : c.second;
         JitEntry* e = nullptr;
-        const int rc2 = get_kernel(p, sp, -1, &e, nullptr);
-        if (getenv("BFA_DEBUG_ROLES")) fprintf(stderr, "role candidate cost %.1f rc %d spill %d\n", c.first, rc2, e ? e->spill : -9);
-        if (rc2 == BFA_OK && e && e->spill == 0) { perm = c.second; break; }
+        if (get_kernel(p, sp, -1, &e, nullptr) == BFA_OK && e && e->spill == 0) { perm = c.second; break; }
       }
     if (!p->opt.jit_cache) {
     } else if (perm.empty()) {
