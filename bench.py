@@ -410,6 +410,19 @@ def run_bfa(args):
         te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = te.item()
+    # for comparison: one cold call with the value plan (long preparation)
+    e2e_value_plan = None
+    if world == 1 and not args.no_extras:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        q = presets.apply(bfa.Program(text), preset, jit_cache=0, **extra_opts)
+        t = q.count_range(n, lo, hi, stream=stream)
+        ok = (int(t.item()) & ((1 << 64) - 1)) == final
+        dt = time.perf_counter() - t0
+        e2e_value_plan = {"s_per_call": dt, "valuations_per_s": (1 << n) / dt, "count_equal": ok,
+                          "what": "one cold call (compile -> count -> host) with the value plan instead of "
+                                  "presets.cold: longer role search and compile, faster kernel"}
+        del q
 
     if rank != 0:
         if world > 1:
@@ -452,7 +465,8 @@ def run_bfa(args):
                         "preparation + one count (presets.cold: role search + PTX compile with the persistent JIT "
                         "cache off, module load, launch) -> count read on the host"
                         + (" -> all-reduce" if world > 1 else ""),
-                "h2d": "the JIT'd cubin loaded into the device each call (count mode has no input tensors)"},
+                "h2d": "the JIT'd cubin loaded into the device each call (count mode has no input tensors)",
+                "value_plan": e2e_value_plan},
         "gpu_launches": launches_timed,
         "kernel_ms_per_step": t_kern * 1e3,
         "prep_s": prep_s,
