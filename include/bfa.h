@@ -168,8 +168,8 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t value);
  * cost: preparation (role searches, decomposition, JIT) + tune_counts x the
  * time of one count (option "tune_counts", default 1 = a single cold count).
  * Tries, in order, (A) the current options as one exhaustive kernel, (B) the
- * kernel-variant sweep (slot bits, inner-loop bits, IMAD/LOP3 balance,
- * register caps: ~18 variants JIT-compiled in parallel and timed on a probe of
+ * kernel-variant sweep (slot bits 2-7, inner-loop bits, IMAD/LOP3 balance,
+ * register caps: ~20 variants JIT-compiled in parallel and timed on a probe of
  * <= 2^36 valuations; only when 30 % of tune_counts x A's count time exceeds
  * its predicted cost), (C) partial evaluation: 2^4 kernel cofactors, then
  * Shannon decompositions into 1024 / 4096 / 16384 / 32768 work-queue leaves;

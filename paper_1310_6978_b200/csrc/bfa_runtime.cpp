@@ -2596,6 +2596,11 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
     c.o.slot_bits = 5; c.o.inner_bits = 4; c.o.dual_pipe = 1; c.o.imad_cost_pct = 35;
     c.o.thread_bits = 7; c.o.min_blocks = 3;
     cands.push_back(c);
+    for (int sb : {6, 7}) {  // more slot cofactors, fewer inner bits (C5 preset: slot 7 / inner 2)
+      Cand d; d.o = o0;
+      d.o.slot_bits = sb; d.o.inner_bits = 9 - sb; d.o.dual_pipe = 1; d.o.imad_cost_pct = 50;
+      cands.push_back(d);
+    }
   }
   const double probe_ms = ms_a * std::ldexp(1.0, kp - k_free);
   const double sweep_est = prep_a * (double)cands.size() / std::min<int>(cores, (int)cands.size()) * 1.5 +
@@ -2670,8 +2675,10 @@ int bfa_autotune_range(bfa_prog* p, int n, int k_free, void* stream, char* repor
       c.o.split_pieces = t.sp;
       c.o.queue_bodies = t.sp ? 512 : 0;
       if (aligned_k(tlo >> 5, hi >> 5) < c.o.decompose_min_k && t.sp) continue;
+      // first estimate per leaf: 1.5 % of the whole program's preparation
+      // (C5: 0.45 s for the whole program, 3.4-5.8 ms per leaf measured)
       const double pred = t.sp == 0 ? prep_a * 16.0 / std::min(16, cores)
-                                    : (per_piece > 0 ? per_piece : 40.0 * prep_a / std::max(1, cores)) * t.sp;
+                                    : (per_piece > 0 ? per_piece : 0.015 * prep_a) * t.sp;
       if (pred >= plans[best].total) {
         char why[160];
         snprintf(why, sizeof why, "predicted preparation %.1f s >= best total %.2f s", pred, plans[best].total);
