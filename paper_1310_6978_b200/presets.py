@@ -23,7 +23,9 @@ about 1.2 s for the 154 ms kernel).
 
 DECOMPOSED: the Reduction applied at preparation time (killing variables /
 "further partition"): a Shannon
-decomposition into 32768 leaves run as persistent work-queue kernels.  Leaves
+decomposition into 16384 leaves run as persistent work-queue kernels with
+slot-7 bodies (0.92 ms per 2^42 after 112 s of preparation; 32768 leaves with
+slot-5 bodies: 1.29 ms after 87 s).  Leaves
 the Reduction proves identically 0 are decided during preparation, so its
 step time is a REPLAY of a prepared plan and is reported as such, next to
 its preparation cost.
@@ -42,8 +44,8 @@ _COLD_BY_CONFIG = {
     "c4": _EXHAUSTIVE_BY_CONFIG["c4"],
 }
 
-DECOMPOSED = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200, role_seeds=1, split_pieces=32768,
-                  queue_bodies=256, queue_inner=2, queue_role_budget=100)
+DECOMPOSED = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200, role_seeds=1, split_pieces=16384,
+                  queue_bodies=256, queue_inner=2, queue_role_budget=100, queue_slot_bits=7)
 
 
 def exhaustive(cfg: str) -> dict:

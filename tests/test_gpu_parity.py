@@ -266,7 +266,7 @@ def test_decomposed_work_queue_vs_oracle():
 
     for qb in (512, 4, 512, 4):
         p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=64, queue_bodies=qb,
-                          decompose_min_k=24, split_min_vars=18)
+                          decompose_min_k=24, split_min_vars=18, queue_slot_bits=5)
         lo = nontrivial_subcube()
         expect = oracle.count(text, n, lo, lo + (1 << 24))
         out = torch.zeros(1, dtype=torch.int64, device="cuda")
@@ -467,7 +467,8 @@ def test_decomposed_body_options_vs_oracle():
         if q.info["const_value"] == -1 and q.info["gates"] >= 150:
             break
     expect = oracle.count(text, n, lo, lo + (1 << 24))
-    for extra in ({"queue_slot_bits": 6, "queue_inner": 1}, {"queue_light_pct": 40, "queue_opt_level": 1}):
+    for extra in ({"queue_slot_bits": 6, "queue_inner": 1},
+                  {"queue_slot_bits": 5, "queue_light_pct": 40, "queue_opt_level": 1}):
         p = presets.apply(bfa.Program(text), presets.DECOMPOSED, split_pieces=64, decompose_min_k=24,
                           split_min_vars=19, **extra)
         assert int(p.count_range(n, lo, lo + (1 << 24)).item()) == expect, extra
@@ -488,7 +489,7 @@ def test_decomposed_large_modules_vs_oracle():
         if q.info["const_value"] == -1 and q.info["gates"] >= 300:
             break
     p = presets.apply(bfa.Program(text), presets.DECOMPOSED, thread_bits=5, split_pieces=2048, split_min_vars=15,
-                      decompose_min_k=24, queue_inner=0)
+                      decompose_min_k=24, queue_inner=0, queue_slot_bits=5)
     expect = oracle.count(text, n, lo, lo + (1 << 26))
     out = torch.zeros(1, dtype=torch.int64, device="cuda")
     for _ in range(4):
@@ -499,8 +500,8 @@ def test_decomposed_large_modules_vs_oracle():
 
 
 def test_decomposed_bench_preset_full_cube():
-    """The bench's replay configuration itself (presets.DECOMPOSED: 32768
-    Shannon leaves in work-queue modules of <= 256 bodies) over the whole C5
+    """The bench's replay configuration itself (presets.DECOMPOSED: 16384
+    Shannon leaves with slot-7 bodies in work-queue modules of <= 256 bodies) over the whole C5
     cube equals the oracle-checked exhaustive kernel's count, replay after
     replay, and f + ~f covers the cube on the exhaustive side (P-11)."""
     text, n, _ = W.config("c5")
@@ -510,7 +511,7 @@ def test_decomposed_bench_preset_full_cube():
     for _ in range(5):
         p.count_range(n, 0, 1 << n, out=out)
         assert int(out.item()) == ref
-    assert bfa.last_launch()["queue"]["bodies"] == 32768
+    assert bfa.last_launch()["queue"]["bodies"] == presets.DECOMPOSED["split_pieces"]
 
 
 def test_concurrent_counts_on_two_streams():
