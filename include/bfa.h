@@ -110,8 +110,12 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   aligned sub-cubes of >= 2^24 valuations (default 1)
  *   "role_budget"   model evaluations of that search (default 200)
  *   "role_seeds"    independent searches (different seeds) of role_budget
- *                   each; the permutation of least modelled cost is kept
- *                   (default 1)
+ *                   each; the permutation of least modelled cost whose
+ *                   compiled kernel spills no registers is kept (default 1)
+ *   "role_seed"     generator seed of the first of those searches (searches
+ *                   use seeds role_seed .. role_seed + role_seeds - 1); the
+ *                   search is deterministic per seed on every host, so a
+ *                   seed measured fastest can be pinned (default 0)
  *   "segment_cells" programs whose cover exceeds 8000 LUTs run as segments of
  *                   this many cells (0 = auto: 768), values crossing segments in
  *                   HBM slot arrays

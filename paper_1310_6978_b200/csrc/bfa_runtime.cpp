@@ -417,6 +417,7 @@ struct Options {
   int role_search = 1;
   int role_budget = 200;
   int role_seeds = 1;            // independent role searches, best modelled cost kept
+  int role_seed = 0;             // first generator seed of those searches (seeds role_seed .. + role_seeds - 1)
   int segment_cells = 0;   // 0: auto (segment when L > 8000), > 0: always, this many cells
   int segment_remat = 2;   // recompute shared cells with cones <= this many cells
   int kernel_cofactor_bits = 0;  // count: split aligned sub-cubes into 2^j cofactor kernels
@@ -535,7 +536,8 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
   spec->perm.clear();
   if (!p->opt.role_search || spec->generic || spec->materialised || spec->mode != bfa::KM_COUNT || k_free < 24) return;
   const std::string key = spec_key(*spec) + "k" + std::to_string(k_free) + "r" + std::to_string(p->opt.role_budget) +
-                          (p->opt.role_seeds > 1 ? "s" + std::to_string(p->opt.role_seeds) : "");
+                          (p->opt.role_seeds > 1 ? "s" + std::to_string(p->opt.role_seeds) : "") +
+                          (p->opt.role_seed ? "o" + std::to_string(p->opt.role_seed) : "");
   {
     std::lock_guard<std::mutex> lk(p->mu);
     auto it = p->roles.find(key);
@@ -563,7 +565,8 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     std::vector<std::pair<double, std::vector<int8_t>>> cand;
     for (int r = 0; r < std::max(1, p->opt.role_seeds); r++) {
       std::vector<int8_t> pm =
-          bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget, 0x13106978ull + 0x9e3779b9ull * r, threads);
+          bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget,
+                            0x13106978ull + 0x9e3779b9ull * (uint64_t)(r + p->opt.role_seed), threads);
       if (p->opt.role_seeds <= 1) { cand.push_back({0.0, pm}); break; }
       bfa::KernelSpec sp = *spec;
       sp.perm = pm;
@@ -1138,7 +1141,7 @@ std::string options_key(const Options& o) {
   std::ostringstream k;
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
-    << ',' << o.role_budget << ',' << o.role_seeds << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
+    << ',' << o.role_budget << ',' << o.role_seeds << ',' << o.role_seed << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
     << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level << ',' << o.queue_slot_bits;
   return k.str();
 }
@@ -2340,6 +2343,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "imad_cost_pct") { if (v < 0 || v > 1000) return bad(); p->opt.imad_cost_pct = (int)v; }
   else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
   else if (k == "role_search") { if (v < 0 || v > 1) return bad(); p->opt.role_search = (int)v; }
+  else if (k == "role_seed") { if (v < 0 || v > 1000000) return bad(); p->opt.role_seed = (int)v; }
   else if (k == "role_budget") { if (v < 1 || v > 4096) return bad(); p->opt.role_budget = (int)v; }
   else if (k == "role_seeds") { if (v < 1 || v > 64) return bad(); p->opt.role_seeds = (int)v; }
   else if (k == "segment_cells") { if (v < 0 || v > 1000000) return bad(); p->opt.segment_cells = (int)v; }

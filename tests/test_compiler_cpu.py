@@ -273,3 +273,22 @@ def test_roles_are_a_permutation_of_the_free_variables():
         assert p.roles(n, k, sms=148) == perm
     with pytest.raises(bfa.BfaError):
         bfa.Program(text).set_option("force_generic", 1).roles(n, n, sms=148)
+
+
+def test_role_seed_is_deterministic_and_selects_the_search():
+    """Option role_seed: the role search of one seed gives the same
+    permutation on every new program object (it is pinned in presets), and
+    another seed searches from another start."""
+    text, n, _ = W.config("c4")
+
+    def perm(seed):
+        p = bfa.Program(text).set_option("slot_bits", 5).set_option("imad_cost_pct", 50)
+        p.set_option("jit_cache", 0).set_option("role_budget", 40).set_option("role_seed", seed)
+        return p.roles(n, n, sms=148)
+
+    a = perm(3)
+    assert sorted(a) == list(range(64))
+    assert perm(3) == a
+    assert any(perm(s) != a for s in (0, 1, 2))
+    with pytest.raises(bfa.BfaError):
+        bfa.Program(text).set_option("role_seed", -1)
