@@ -529,9 +529,42 @@ def run_extras(args, bfa, presets, torch, stream, dev, text, n, final, verified,
         verified["c4_closed_form"] = int(c4.item()) == e4
         out["c4_exhaustive"] = {"valuations_per_s": (1 << n4) / t, "ms_per_step": t * 1e3, "count": int(c4.item()),
                                 "roofline": int_roofline(l4, 1 << (n4 - 5), t, peaks, "c4_exhaustive")}
+        out["c4_eval"] = eval_line(bfa, torch, stream, dev, p4, n4, e4, max(args.steps, 5), timer, verified)
+        del p4
         for name in ("c2", "c2_fused", "c2_n32", "c2_n32_fused"):
             out[name] = materialised_line(bfa, torch, stream, name, 3, timer)
     return out
+
+
+def eval_line(bfa, torch, stream, dev, prog, n, expect, steps, timer, verified):
+    """Register-mode eval (bfa_eval_range, Prop 2.2): the
+    full 2^n-bit DNF vector written to HBM (C4: 2^36 bits = 8 GiB) with the
+    fused popcount.  Bound by the 2^n/8 bytes of stores (SURVEY §8(d):
+    register eval = the count's cells + 2^n/8 bytes written)."""
+    vec = torch.empty(bfa.words_for(n), dtype=torch.int64, device=dev)
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    for _ in range(2):
+        prog.eval_range(n, 0, 1 << n, out=vec, count_out=cnt, stream=stream)
+    torch.cuda.synchronize()
+    launch = bfa.last_launch()
+    ts = timer.run(lambda: prog.eval_range(n, 0, 1 << n, out=vec, count_out=cnt, stream=stream), steps)
+    t = statistics.median(ts)
+    c = int(cnt.item())
+    pc = torch.zeros(1, dtype=torch.int64, device=dev)
+    bfa.popcount(vec, count_out=pc, stream=stream)
+    torch.cuda.synchronize()
+    verified["c4_eval_count"] = c == expect and int(pc.item()) == expect
+    del vec
+    torch.cuda.empty_cache()
+    written = (1 << n) // 8
+    peak, src = hbm_peak()
+    return {"valuations_per_s": (1 << n) / t, "ms_per_step": t * 1e3, "count": c,
+            "vector_popcount": int(pc.item()), "vector_bytes": written,
+            "roofline": {"bound": "hbm", "achieved": written / t / 1e9, "peak": peak / 1e9, "unit": "GB/s",
+                         "frac": written / t / peak, "peak_source": src + " (read+write copy; this kernel only writes)",
+                         "traffic": None, "per_unit": "2^n/8 bytes of vector stores per step, no loads"},
+            "kernels": launch.get("kernels"),
+            "what": "full-DNF vector of C4 (2^36 bits) in HBM + fused popcount, one register-mode eval kernel"}
 
 
 def hbm_peak():

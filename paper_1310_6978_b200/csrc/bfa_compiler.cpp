@@ -879,6 +879,14 @@ static void build_specialised(const Parsed& prog, const KernelSpec& spec, Built*
   const int s = b->s, t = b->t, m = b->m;
   b->pos.resize(64);
   for (int v = 0; v < 64; v++) b->pos[v] = (v < (int)spec.perm.size()) ? spec.perm[v] : v;
+  if (spec.mode == KM_EVAL && !spec.generic && spec.vec_bits >= 0 && spec.vec_bits < s) {
+    // eval store layout: word-index bit w of variable 5 + w holds slot bit w
+    // (w < a), thread bit w - a (a <= w < a + t), slot bit w - t (a + t <= w
+    // < s + t); every higher bit keeps its position
+    const int a = spec.vec_bits;
+    for (int w = 0; w < s + t && 5 + w < 64; w++)
+      b->pos[5 + w] = 5 + (w < a ? w : w < a + t ? s + (w - a) : w - t);
+  }
   // roles of word-index bit p = pos(v) - 5:
   //   generic:     every v >= 5 is level 3, read from w
   //   specialised: p < s slot (constant per slot), < s+t thread (1),
@@ -1366,13 +1374,21 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
     emit_level(3, "      ");
     for (int sl = 0; sl < S; sl++) os << "      const u32 r" << sl << " = " << E.value(outs[sl]) << ";\n";
     if (spec.mode == KM_EVAL) {
-      os << "      const u64 idx = (wo - out_base_w) + ((u64)i << " << (s + t) << ") + ((u64)tid << " << s << ");\n";
-      if (S == 1) os << "      out[idx] = r0;\n";
-      else if (S == 2) os << "      *reinterpret_cast<u32x2*>(out + idx) = u32x2{r0, r1};\n";
-      else
-        for (int g = 0; g < S; g += 4)
-          os << "      *reinterpret_cast<u32x4*>(out + idx + " << g << ") = u32x4{r" << g << ", r" << g + 1
-             << ", r" << g + 2 << ", r" << g + 3 << "};\n";
+      // slot sl -> word (sl & (2^a - 1)) + (tid << a) + ((sl >> a) << (a + t))
+      // of the inner iteration's 2^(s+t) words (build_specialised's layout)
+      const int a = (spec.vec_bits >= 0 && spec.vec_bits < s) ? spec.vec_bits : s;
+      const int V = 1 << a;
+      os << "      const u64 idx = (wo - out_base_w) + ((u64)i << " << (s + t) << ") + ((u64)tid << " << a << ");\n";
+      for (int g = 0; g < S; g += V) {
+        const uint64_t off = (uint64_t)(g >> a) << (a + t);
+        if (V == 1) os << "      out[idx + " << off << "ull] = r" << g << ";\n";
+        else if (V == 2)
+          os << "      *reinterpret_cast<u32x2*>(out + idx + " << off << "ull) = u32x2{r" << g << ", r" << g + 1 << "};\n";
+        else
+          for (int h = 0; h < V; h += 4)
+            os << "      *reinterpret_cast<u32x4*>(out + idx + " << off + h << "ull) = u32x4{r" << g + h << ", r"
+               << g + h + 1 << ", r" << g + h + 2 << ", r" << g + h + 3 << "};\n";
+      }
     }
     if (want_count) {
       os << "      acc32 += ";

@@ -143,6 +143,12 @@ struct KernelSpec {
                               // model_cost -- the role search's objective -- uses 0)
   int count_shift = 0;        // count mode: the count is scaled by 2^count_shift
                               // (support reduction: variables outside the support)
+  int vec_bits = -1;          // eval mode: each thread stores 2^vec_bits consecutive
+                              // words per vector store; the slot bits above
+                              // vec_bits sit above the thread bits in the word
+                              // index, so a warp's store covers 32 x 2^vec_bits
+                              // consecutive words (-1 or >= s: all s slot bits
+                              // below the thread bits)
 };
 
 struct KernelStats {

@@ -517,6 +517,7 @@ std::string spec_key(const bfa::KernelSpec& s) {
   k << s.mode << (s.generic ? 'g' : 's') << s.slot_bits << '.' << s.thread_bits << '.' << s.inner_bits
     << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-') << 'd' << s.dual_pipe << '.' << s.imad_cost_pct << 'b' << s.min_blocks;
   if (s.count_shift) k << 'x' << s.count_shift;
+  if (s.vec_bits >= 0) k << 'v' << s.vec_bits;
   if (!s.perm.empty()) {
     k << 'p';
     for (int8_t q : s.perm) k << (char)('0' + q);
@@ -881,12 +882,16 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
   }
   // full-chip grid estimate for planning (exact occupancy comes from the kernel)
   const int full_grid = di.sms * std::max(1, o.blocks_per_sm ? o.blocks_per_sm : 2048 / T / 2);
-  // eval stores 2^s consecutive words per thread as one vector store: the
-  // slice's word 0 must sit at a (4 * 2^s)-byte aligned address relative to
-  // the unit grid, else use narrower slots.
-  int s_eff = eval ? std::min(o.slot_bits, 5) : o.slot_bits;   // eval stores <= 32 words per thread-iteration
+  // eval: each thread stores its slot words in vectors of 2^a consecutive
+  // words (a <= 2: 16 B), the slot bits above a sitting above the thread bits,
+  // so one warp store instruction writes 32 x 2^a consecutive words
+  // (coalesced); the slice's word 0 must sit at a (4 * 2^a)-byte aligned
+  // address relative to the unit grid, else narrower vectors.  At most 2^5
+  // slot words per thread-iteration (all stay live until the stores).
+  int s_eff = eval ? std::min(o.slot_bits, 5) : o.slot_bits;
+  int a_eff = std::min(s_eff, 2);
   if (eval)
-    while (s_eff > 0 && ((reinterpret_cast<uintptr_t>(out_dev) - 4 * (uintptr_t)wlo) & ((4u << s_eff) - 1))) s_eff--;
+    while (a_eff > 0 && ((reinterpret_cast<uintptr_t>(out_dev) - 4 * (uintptr_t)wlo) & ((4u << a_eff) - 1))) a_eff--;
   std::vector<Segment> segs = plan(o, s_eff, n, wlo, whi, full_grid);
   std::ostringstream js;
   js << "{\"device\": " << dev << ", \"sms\": " << di.sms << ", \"segments\": [";
@@ -901,6 +906,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
     spec.thread_bits = o.thread_bits;
     spec.inner_bits = sg.generic ? 0 : sg.m;
     spec.fuse_count = eval && count_dev != nullptr;
+    spec.vec_bits = eval && !sg.generic ? a_eff : -1;
     spec.dual_pipe = o.dual_pipe;
     spec.imad_cost_pct = o.imad_cost_pct;
     spec.min_blocks = sg.generic ? 0 : o.min_blocks;
@@ -2144,6 +2150,10 @@ int spec_for_what(const bfa_prog* p, int what, bfa::KernelSpec* spec) {
   spec->dual_pipe = p->opt.dual_pipe;
   spec->imad_cost_pct = p->opt.imad_cost_pct;
   spec->min_blocks = spec->generic ? 0 : p->opt.min_blocks;
+  if (what == 2) {  // as run_range launches it on a 16-byte aligned slice
+    spec->slot_bits = std::min(spec->slot_bits, 5);
+    spec->vec_bits = std::min(spec->slot_bits, 2);
+  }
   return BFA_OK;
 }
 
