@@ -558,11 +558,13 @@ def eval_line(bfa, torch, stream, dev, prog, n, expect, steps, timer, verified):
     torch.cuda.empty_cache()
     written = (1 << n) // 8
     peak, src = hbm_peak()
+    dram = traffic_for("c4_eval")
     return {"valuations_per_s": (1 << n) / t, "ms_per_step": t * 1e3, "count": c,
             "vector_popcount": int(pc.item()), "vector_bytes": written,
             "roofline": {"bound": "hbm", "achieved": written / t / 1e9, "peak": peak / 1e9, "unit": "GB/s",
                          "frac": written / t / peak, "peak_source": src + " (read+write copy; this kernel only writes)",
-                         "traffic": None, "per_unit": "2^n/8 bytes of vector stores per step, no loads"},
+                         "traffic": dram, "dram_frac": (dram / t / peak) if dram else None,
+                         "per_unit": "2^n/8 bytes of vector stores per step, no loads"},
             "kernels": launch.get("kernels"),
             "what": "full-DNF vector of C4 (2^36 bits) in HBM + fused popcount, one register-mode eval kernel"}
 

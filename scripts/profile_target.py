@@ -1,7 +1,7 @@
 """Profiling targets for ncu (one GPU): the bench's kernels, launched as the
 bench launches them, `steps` times (ncu -s/-c pick the launches).
 
-    python scripts/profile_target.py exhaustive|c4_exhaustive|replay|materialised [steps]
+    python scripts/profile_target.py exhaustive|c4_exhaustive|replay|materialised|c4_eval [steps]
 """
 import os
 import sys
@@ -23,6 +23,14 @@ if what in ("exhaustive", "c4_exhaustive", "replay"):
     p = presets.apply(bfa.Program(text), preset)
     for _ in range(steps):
         p.count_range(n, 0, 1 << n, out=cnt)
+    torch.cuda.synchronize()
+    print(what, int(cnt.item()), bfa.last_launch())
+elif what == "c4_eval":
+    text, n, _ = W.config("c4")
+    p = presets.apply(bfa.Program(text), presets.exhaustive("c4"))
+    vec = torch.empty(bfa.words_for(n), dtype=torch.int64, device="cuda")
+    for _ in range(steps):
+        p.eval_range(n, 0, 1 << n, out=vec, count_out=cnt)
     torch.cuda.synchronize()
     print(what, int(cnt.item()), bfa.last_launch())
 elif what == "materialised":
