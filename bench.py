@@ -454,6 +454,12 @@ def run_bfa(args):
                           if args.share_device and world > 1 else {})),
         "program": {"gates_G": info["gates"], "luts_L": info["luts"], "support": info["support"],
                     "options": dict(preset, **extra_opts)},
+        "gate_word_ops": {
+            "nominal_per_s": info["gates"] * value / 32, "lut3_level_per_s": info["luts"] * value / 32,
+            "lop3_peak_per_s": peaks["lop3"],
+            "note": "SURVEY 8(d): G (gates) and L (LUT3 cells of the unspecialised cover) x 32-bit words per "
+                    "second. Both exceed the LOP3 peak: slot cofactoring and loop hoisting execute "
+                    "roofline.per_unit cells per word instead of L, so they are nominal, not executed, rates"},
         "count": final, "count_expected": expect, "count_verified": verified,
         "decided_at_compile_time": 0,
         "roofline": roof,
