@@ -105,6 +105,11 @@ int bfa_info_get(const bfa_prog* p, bfa_info* out);
  *                   FMA pipe next to LOP3 cells on the ALU pipe (default 1)
  *   "imad_cost_pct" IMAD:LOP3 cost ratio in percent for that mapping, 0 = model
  *                   sweep (default 0)
+ *   "imad_pairs"    count mode: an inner-loop LOP3 cell whose other two inputs
+ *                   are hoisted word-uniform values becomes x * K + C on the
+ *                   FMA pipe (K, C: LOP3 cells at the hoisted level) while the
+ *                   modelled ALU work exceeds the FMA work; 2 = roles searched
+ *                   without it, kernel emitted with it (default 0)
  *   "min_blocks"    __launch_bounds__ minimum blocks per SM, 0 = none (default 0)
  *   "role_search"   1 = count mode searches the variable -> bit-position roles on
  *                   aligned sub-cubes of >= 2^24 valuations (default 1)

@@ -818,6 +818,11 @@ struct Emitter {
            << ") : \"r\"(" << name(L.in[0]) << "), " << affine(L.in[1], m0 - m1, m0, false) << ", "
            << affine(L.in[1], c0 - c1, c0, false) << ");\n";
       }
+    } else if (L.kind == 2) {  // x * K + C (K, C hoisted; a constant x goes in the immediate slot)
+      const bool xc = d.nodes[L.in[0]].kind == NK_CONST;
+      os << indent << "u32 " << name(L.root) << "; asm(\"mad.lo.u32 %0, %1, %2, %3;\" : \"=r\"(" << name(L.root)
+         << ") : " << operand(xc ? L.in[1] : L.in[0]) << ", " << operand(xc ? L.in[0] : L.in[1]) << ", "
+         << operand(L.in[2]) << ");\n";
     } else {
       char immb[8];
       snprintf(immb, sizeof immb, "0x%02x", L.imm);
@@ -939,7 +944,8 @@ static double model_time(const Built& b, const MapResult& r, const KernelSpec& s
     derived.push_back((uint64_t)u << 16 | (uint64_t)(k + 8) << 8 | (uint64_t)(c + 8));
   };
   for (const Lut& L : r.luts) {
-    if (L.kind != 1) { A += b.w[L.level]; continue; }
+    if (L.kind == 0) { A += b.w[L.level]; continue; }
+    if (L.kind == 2) { F += b.w[L.level]; continue; }
     F += b.w[L.level];
     if (b.D.nodes[L.in[0]].kind == NK_CONST) continue;
     int m0, c0, m1, c1;
@@ -1001,7 +1007,123 @@ static double model_time(const Built& b, const MapResult& r, const KernelSpec& s
 // may become IMAD cells (FMA pipe) instead of being absorbed into LOP3 cells
 // (ALU pipe); sweep the IMAD:LOP3 cost ratio (or use the fixed one) and keep
 // the cover with the least modelled time.
-static MapResult choose_mapping(const Built& b, const KernelSpec& spec, double* best_time, double* chosen) {
+// Kind-2 IMAD cells (KernelSpec::imad_pairs).  An inner-loop LOP3 cell
+// g(x, u1, u2) whose leaves u1, u2 are word-uniform (0 or ~0 in every word)
+// and hoisted (thread / outer level) is, for each value of (u1, u2), one of
+// the unary functions 0, ~0, x, ~x of x, i.e. x * K + C with K in {0, 1, -1}
+// and C in {0, -1} functions of (u1, u2): one IMAD on the FMA pipe in the
+// inner loop.  K = lop3(u1, u2, 0xFFFFFFFE) (bit 0: K != 0; bits 1..31:
+// K == -1) and C = lop3(u1, u2) are cells at the hoisted level, shared
+// between cells.  Cells are converted while the modelled ALU work exceeds
+// the FMA work (model_time's pipe balance); the new nodes are appended to
+// b.D outside the hash-consing tables.
+static void imad_pairs(Built& b, MapResult& r) {
+  Dag& D = b.D;
+  const size_t N0 = D.nodes.size();
+  std::vector<uint8_t> uniform(N0, 0);
+  for (size_t n = 0; n < N0; n++) {
+    const Node& nd = D.nodes[n];
+    if (nd.kind == NK_VAR) uniform[n] = 1;
+    else if (nd.kind == NK_CONST) uniform[n] = n == 0;
+    else uniform[n] = uniform[nd.a] && uniform[nd.b];
+  }
+  double A = 0, F = 0;
+  for (const Lut& L : r.luts) (L.kind == 0 ? A : F) += b.w[L.level];
+  const double other = b.S + b.S / 2.0 + 2.0 + 2.0 * b.m;
+  auto new_node = [&](NodeKind k, uint32_t a, uint32_t c, uint32_t val, uint8_t level) {
+    D.nodes.push_back(Node{k, 0, a, c, val});
+    r.node_level.push_back(level);
+    return (uint32_t)(D.nodes.size() - 1);
+  };
+  std::map<std::tuple<uint32_t, uint32_t, int, int>, uint32_t> made;  // (u1, u2, K/C, tt) -> node
+  uint32_t not_one = UINT32_MAX;
+  std::vector<Lut> added;
+  for (Lut& L : r.luts) {
+    if (F + 2.0 > A + other) break;  // pipes balanced
+    if (L.kind != 0 || L.level != 3 || L.nin != 3) continue;
+    int ix = -1, nu = 0;
+    for (int q = 0; q < 3; q++)
+      if (!uniform[L.in[q]]) { ix = q; nu++; }
+    if (nu != 1) continue;
+    int iu[2], k = 0;
+    for (int q = 0; q < 3; q++)
+      if (q != ix) iu[k++] = q;
+    const uint32_t u1 = L.in[iu[0]], u2 = L.in[iu[1]], x = L.in[ix];
+    if (u1 == u2 || D.nodes[u1].kind == NK_CONST || D.nodes[u2].kind == NK_CONST) continue;
+    const uint8_t lv = std::max(r.node_level[u1], r.node_level[u2]);
+    if (lv >= 3) continue;
+    int m[4], c[4];
+    for (int pq = 0; pq < 4; pq++) {
+      int v[2];
+      for (int xv = 0; xv < 2; xv++) {
+        int bits[3];
+        bits[ix] = xv;
+        bits[iu[0]] = pq & 1;
+        bits[iu[1]] = pq >> 1;
+        v[xv] = (L.imm >> (bits[0] * 4 + bits[1] * 2 + bits[2])) & 1;
+      }
+      Emitter::mc(unary_code(v[0], v[1]), &m[pq], &c[pq]);
+    }
+    const bool kconst = m[0] == m[1] && m[0] == m[2] && m[0] == m[3];
+    const bool cconst = c[0] == c[1] && c[0] == c[2] && c[0] == c[3];
+    const bool xconst = D.nodes[x].kind == NK_CONST;
+    if (kconst && (m[0] == 0 || xconst)) continue;
+    double dA = 0;
+    uint32_t kn, cn;
+    if (kconst) {
+      kn = new_node(NK_CONST, 0, 0, (uint32_t)m[0], 0);
+    } else {
+      int tt = 0;
+      for (int a = 0; a < 2; a++)
+        for (int bb = 0; bb < 2; bb++)
+          for (int cb = 0; cb < 2; cb++) {
+            const int pq = a | bb << 1;
+            if (cb == 0 ? m[pq] != 0 : m[pq] == -1) tt |= 1 << (a * 4 + bb * 2 + cb);
+          }
+      auto it = made.find({u1, u2, 0, tt});
+      if (it != made.end()) {
+        kn = it->second;
+      } else {
+        if (not_one == UINT32_MAX) not_one = new_node(NK_CONST, 0, 0, 0xFFFFFFFEu, 0);
+        kn = new_node(NK_GATE, u1, u2, 0, lv);
+        Lut K{};
+        K.root = kn; K.nin = 3; K.in[0] = u1; K.in[1] = u2; K.in[2] = not_one; K.imm = (uint8_t)tt; K.level = lv;
+        added.push_back(K);
+        made[{u1, u2, 0, tt}] = kn;
+        dA += b.w[lv];
+      }
+    }
+    if (cconst) {
+      cn = c[0] == 0 ? 0u : new_node(NK_CONST, 0, 0, 0xFFFFFFFFu, 0);
+    } else {
+      int tt = 0;
+      for (int a = 0; a < 2; a++)
+        for (int bb = 0; bb < 2; bb++)
+          if (c[a | bb << 1] == -1) tt |= 1 << (a * 4 + bb * 2) | 1 << (a * 4 + bb * 2 + 1);
+      auto it = made.find({u1, u2, 1, tt});
+      if (it != made.end()) {
+        cn = it->second;
+      } else {
+        cn = new_node(NK_GATE, u1, u2, 0, lv);
+        Lut C{};
+        C.root = cn; C.nin = 2; C.in[0] = u1; C.in[1] = u2; C.in[2] = u1; C.imm = (uint8_t)tt; C.level = lv;
+        added.push_back(C);
+        made[{u1, u2, 1, tt}] = cn;
+        dA += b.w[lv];
+      }
+    }
+    L.kind = 2;
+    L.nin = 3;
+    L.in[0] = x;
+    L.in[1] = kn;
+    L.in[2] = cn;
+    A += dA - 1.0;
+    F += 1.0;
+  }
+  for (const Lut& L : added) r.luts.push_back(L);
+}
+
+static MapResult choose_mapping(Built& b, const KernelSpec& spec, double* best_time, double* chosen) {
   MapResult mr;
   double best = 1e300, cost = 0.0;
   std::vector<double> sweep = {0.0};
@@ -1009,8 +1131,10 @@ static MapResult choose_mapping(const Built& b, const KernelSpec& spec, double* 
     if (spec.imad_cost_pct > 0) sweep = {spec.imad_cost_pct / 100.0};
     else sweep = {0.0, 0.6, 0.75, 0.9, 1.0, 1.15, 1.3, 1.6, 2.0, 3.0};
   }
+  const bool pairs = spec.imad_pairs && spec.dual_pipe && spec.mode == KM_COUNT && !spec.generic && !spec.materialised;
   for (double c : sweep) {
     MapResult r = map_luts(b.D, b.outs, b.var_level, b.w, c, spec.area_passes);
+    if (pairs) imad_pairs(b, r);
     double tm = model_time(b, r, spec);
     if (tm < best - 1e-9) { best = tm; mr = std::move(r); cost = c; }
   }
@@ -1276,7 +1400,7 @@ std::string emit_kernel(const Parsed& prog, const KernelSpec& spec, KernelStats*
       E.lut(L, ind);
       uint32_t* luts = lvl == 1 ? &st.luts_thread : lvl == 2 ? &st.luts_outer : &st.luts_inner;
       uint32_t* imads = lvl == 1 ? &st.imads_thread : lvl == 2 ? &st.imads_outer : &st.imads_inner;
-      (*(L.kind == 1 ? imads : luts))++;
+      (*(L.kind != 0 ? imads : luts))++;
     }
   };
   auto declare_var = [&](int v, const std::string& expr, const char* ind) {
@@ -1486,6 +1610,10 @@ struct PtxEmitter {
         os << "\tmad.lo.u32 " << reg(L.root) << ", " << reg(L.in[0]) << ", " << affine(L.in[1], m0 - m1, m0, false)
            << ", " << affine(L.in[1], c0 - c1, c0, false) << ";\n";
       }
+    } else if (L.kind == 2) {  // x * K + C (K, C hoisted; a constant x goes in the immediate slot)
+      const bool xc = d.nodes[L.in[0]].kind == NK_CONST;
+      os << "\tmad.lo.u32 " << reg(L.root) << ", " << operand(xc ? L.in[1] : L.in[0]) << ", "
+         << operand(xc ? L.in[0] : L.in[1]) << ", " << operand(L.in[2]) << ";\n";
     } else {
       char imm[8];
       snprintf(imm, sizeof imm, "0x%02X", L.imm);
@@ -1569,7 +1697,7 @@ std::string emit_ptx(const Parsed& prog, const KernelSpec& spec, KernelStats* st
       E.cell(L);
       uint32_t* luts = lvl == 1 ? &st.luts_thread : lvl == 2 ? &st.luts_outer : &st.luts_inner;
       uint32_t* imads = lvl == 1 ? &st.imads_thread : lvl == 2 ? &st.imads_outer : &st.imads_inner;
-      (*(L.kind == 1 ? imads : luts))++;
+      (*(L.kind != 0 ? imads : luts))++;
       if (lvl == 3 && out_use.count(L.root)) count_out(L.root, "%a32");
     }
   };

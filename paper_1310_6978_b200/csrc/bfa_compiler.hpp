@@ -102,6 +102,10 @@ struct Lut {
   // kind 1 = IMAD cell (FMA pipe): root = u ? f1(x) : f0(x) with x = in[0] and
   // u = in[1] a word-uniform value (0 or ~0 in every word); f0/f1 are unary
   // codes 0:"0", 1:"~0", 2:"x", 3:"~x"; emitted as x * M(u) + C(u).
+  // kind 2 = IMAD cell of a 3-input cut with two word-uniform leaves:
+  // root = x * in[1] + in[2] (mad.lo.u32), in[1] = K(u1, u2) in {0, 1, ~0}
+  // and in[2] = C(u1, u2) in {0, ~0} computed by LOP3 cells at the uniform
+  // leaves' (hoisted) loop level (KernelSpec::imad_pairs).
   uint8_t kind = 0;
   uint8_t f0 = 0, f1 = 0;
 };
@@ -143,6 +147,9 @@ struct KernelSpec {
                               // model_cost -- the role search's objective -- uses 0)
   int count_shift = 0;        // count mode: the count is scaled by 2^count_shift
                               // (support reduction: variables outside the support)
+  int imad_pairs = 0;         // count mode: inner-loop LOP3 cells whose other two
+                              // leaves are hoisted word-uniform values become
+                              // kind-2 IMAD cells while that balances the pipes
   int vec_bits = -1;          // eval mode: each thread stores 2^vec_bits consecutive
                               // words per vector store; the slot bits above
                               // vec_bits sit above the thread bits in the word

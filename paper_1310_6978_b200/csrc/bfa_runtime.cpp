@@ -413,6 +413,7 @@ struct Options {
   int engine = 0;
   int dual_pipe = 1;
   int imad_cost_pct = 0;
+  int imad_pairs = 0;            // count mode: kind-2 IMAD cells (two hoisted uniform leaves)
   int min_blocks = 0;
   int role_search = 1;
   int role_budget = 200;
@@ -518,6 +519,7 @@ std::string spec_key(const bfa::KernelSpec& s) {
     << (s.fuse_count ? 'f' : '-') << (s.materialised ? 'M' : '-') << 'd' << s.dual_pipe << '.' << s.imad_cost_pct << 'b' << s.min_blocks;
   if (s.count_shift) k << 'x' << s.count_shift;
   if (s.vec_bits >= 0) k << 'v' << s.vec_bits;
+  if (s.imad_pairs) k << 'q';
   if (!s.perm.empty()) {
     k << 'p';
     for (int8_t q : s.perm) k << (char)('0' + q);
@@ -565,8 +567,10 @@ void resolve_roles(const bfa_prog* cp, bfa::KernelSpec* spec, int k_free) {
     // can spill and run 1.6x slower), else the cheapest
     std::vector<std::pair<double, std::vector<int8_t>>> cand;
     for (int r = 0; r < std::max(1, p->opt.role_seeds); r++) {
+      bfa::KernelSpec search_spec = *spec;
+      if (search_spec.imad_pairs == 2) search_spec.imad_pairs = 0;  // search without, emit with
       std::vector<int8_t> pm =
-          bfa::search_roles(p->parsed, *spec, k_free, p->opt.role_budget,
+          bfa::search_roles(p->parsed, search_spec, k_free, p->opt.role_budget,
                             0x13106978ull + 0x9e3779b9ull * (uint64_t)(r + p->opt.role_seed), threads);
       if (p->opt.role_seeds <= 1) { cand.push_back({0.0, pm}); break; }
       bfa::KernelSpec sp = *spec;
@@ -909,6 +913,7 @@ int run_range_core(const bfa_prog* p, int n, uint64_t mu_lo, uint64_t mu_hi, uin
     spec.vec_bits = eval && !sg.generic ? a_eff : -1;
     spec.dual_pipe = o.dual_pipe;
     spec.imad_cost_pct = o.imad_cost_pct;
+    spec.imad_pairs = eval ? 0 : o.imad_pairs;
     spec.min_blocks = sg.generic ? 0 : o.min_blocks;
     // force_roles_k (autotune probes only): time the kernel whose roles were
     // searched for a larger sub-cube; its count over this range is not used.
@@ -976,7 +981,7 @@ int cube_spec(const bfa_prog* p, int n, int k_free, int sms, bfa::KernelSpec* sp
     if (sg.generic) continue;
     spec->mode = bfa::KM_COUNT; spec->generic = false; spec->slot_bits = o.slot_bits;
     spec->thread_bits = o.thread_bits; spec->inner_bits = sg.m; spec->dual_pipe = o.dual_pipe;
-    spec->imad_cost_pct = o.imad_cost_pct; spec->min_blocks = o.min_blocks;
+    spec->imad_cost_pct = o.imad_cost_pct; spec->min_blocks = o.min_blocks; spec->imad_pairs = o.imad_pairs;
     resolve_roles(p, spec, k_free);
     return BFA_OK;
   }
@@ -1059,7 +1064,7 @@ int prepare_count(const bfa_prog* p, int n, int sms) {
     bfa::KernelSpec spec;
     spec.mode = bfa::KM_COUNT; spec.generic = false; spec.slot_bits = o.slot_bits; spec.thread_bits = o.thread_bits;
     spec.inner_bits = sg.m; spec.dual_pipe = o.dual_pipe; spec.imad_cost_pct = o.imad_cost_pct;
-    spec.min_blocks = o.min_blocks;
+    spec.min_blocks = o.min_blocks; spec.imad_pairs = o.imad_pairs;
     resolve_roles(p, &spec, aligned_k(sg.wb, sg.we));
     int rc = get_kernel(p, spec, -1, nullptr, nullptr);
     if (rc) return rc;
@@ -1147,7 +1152,7 @@ std::string options_key(const Options& o) {
   std::ostringstream k;
   k << o.slot_bits << ',' << o.thread_bits << ',' << o.inner_bits << ',' << o.blocks_per_sm << ',' << o.force_generic
     << ',' << o.engine << ',' << o.dual_pipe << ',' << o.imad_cost_pct << ',' << o.min_blocks << ',' << o.role_search
-    << ',' << o.role_budget << ',' << o.role_seeds << ',' << o.role_seed << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
+    << ',' << o.role_budget << ',' << o.role_seeds << ',' << o.role_seed << ',' << o.imad_pairs << ',' << o.segment_cells << ',' << o.segment_remat << ',' << o.kernel_cofactor_bits << ','
     << o.split_pieces << ',' << o.streams << ',' << o.multi_body << ',' << o.split_policy << ',' << o.queue_bodies << ',' << o.queue_chunk << ',' << o.queue_inner << ',' << o.queue_support << ',' << o.split_merge << ',' << o.queue_role_budget << ',' << o.decompose_min_k << ',' << o.split_min_vars << ',' << o.ptx << ',' << o.queue_light_pct << ',' << o.queue_opt_level << ',' << o.queue_slot_bits;
   return k.str();
 }
@@ -1252,7 +1257,7 @@ int ensure_multi(bfa_prog* mp, const std::string& kkey, std::vector<std::unique_
     bfa::KernelSpec base;
     base.mode = bfa::KM_COUNT; base.generic = false; base.slot_bits = o.slot_bits; base.thread_bits = o.thread_bits;
     base.inner_bits = segs[0].m; base.dual_pipe = o.dual_pipe; base.imad_cost_pct = o.imad_cost_pct;
-    base.min_blocks = o.min_blocks;
+    base.min_blocks = o.min_blocks; base.imad_pairs = o.imad_pairs;
     std::vector<bfa::KernelSpec> specs(live.size(), base);
     {  // role searches in parallel (cached per child and on disk)
       std::vector<std::thread> th;
@@ -2149,6 +2154,7 @@ int spec_for_what(const bfa_prog* p, int what, bfa::KernelSpec* spec) {
   spec->inner_bits = spec->generic ? 0 : p->opt.inner_bits;
   spec->dual_pipe = p->opt.dual_pipe;
   spec->imad_cost_pct = p->opt.imad_cost_pct;
+  spec->imad_pairs = what == 1 ? p->opt.imad_pairs : 0;
   spec->min_blocks = spec->generic ? 0 : p->opt.min_blocks;
   if (what == 2) {  // as run_range launches it on a 16-byte aligned slice
     spec->slot_bits = std::min(spec->slot_bits, 5);
@@ -2350,6 +2356,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   else if (k == "force_generic") { if (v < 0 || v > 1) return bad(); p->opt.force_generic = (int)v; }
   else if (k == "engine") { if (v < 0 || v > 1) return bad(); p->opt.engine = (int)v; }
   else if (k == "dual_pipe") { if (v < 0 || v > 1) return bad(); p->opt.dual_pipe = (int)v; }
+  else if (k == "imad_pairs") { if (v < 0 || v > 2) return bad(); p->opt.imad_pairs = (int)v; }
   else if (k == "imad_cost_pct") { if (v < 0 || v > 1000) return bad(); p->opt.imad_cost_pct = (int)v; }
   else if (k == "min_blocks") { if (v < 0 || v > 32) return bad(); p->opt.min_blocks = (int)v; }
   else if (k == "role_search") { if (v < 0 || v > 1) return bad(); p->opt.role_search = (int)v; }

@@ -305,6 +305,26 @@ def test_role_search_subcubes():
         assert a + b == 1 << k
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("pairs", [1, 2])
+def test_imad_pair_cells_vs_oracle(pairs):
+    """Option imad_pairs (kind-2 IMAD cells x * K(u1, u2) + C(u1, u2), K and C
+    hoisted LOP3 cells): the whole-cube C5 kernel built with it, run by
+    bfa_count_positions on 2 ranges of 2^24 positions of its enumeration
+    order, against the oracle on the renamed program (PAPER.md:341-354 Prop
+    2.2); C4's full cube gives the closed form 130023 (OEIS A001035)."""
+    text, n, _ = W.config("c5")
+    p = presets.apply(bfa.Program(text), presets.exhaustive("c5"), role_seeds=1, imad_pairs=pairs)
+    text2 = renamed(text, p.roles(n))
+    for lo in ((77 << 24), (1 << 42) - (1 << 24)):
+        got = int(p.count_positions(n, n, lo, lo + (1 << 24)).item())
+        assert got == oracle.count(text2, n, lo, lo + (1 << 24)), (pairs, lo)
+    t4, n4, e4 = W.config("c4")
+    q = presets.apply(bfa.Program(t4), presets.exhaustive("c4"), imad_pairs=pairs)
+    assert q.count(n4) == e4
+
+
+@pytest.mark.gpu
 def test_kernel_cofactoring():
     """Kernel-level cofactoring (2^j cofactor programs via bfa_assume, each
     with its own role search and kernel, constant-0 cofactors decided at
