@@ -232,6 +232,19 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def ncu_alu_for(cfg):
+    """ALU-pipe utilisation of the kernel from the committed ncu --set full
+    capture (profiles/traffic.json): SURVEY 8(d)'s executed-instruction
+    fraction (every ALU-pipe instruction, loop and popcount included), next
+    to the cover-cell fraction measured live."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            e = json.load(f)[cfg]
+        return dict(e["ncu_alu_pipe"], source=e["source"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def traffic_for(cfg):
     """DRAM bytes per launch of the dominant kernel from the committed ncu
     --set full capture (profiles/traffic.json), or None."""
@@ -286,6 +299,7 @@ def int_roofline(launch, words, seconds, peaks, cfg):
             "peak_source": "measured bfa_peak_int rates (LOP3 ALU pipe, IMAD FMA pipe, 1:1 mix issue-bound); "
                            "peak = the binding pipe for this kernel's LOP3:IMAD mix",
             "peak_measured": peaks,
+            "ncu_alu_pipe": ncu_alu_for(cfg),
             "alu_pipe": {"lop3_per_s": A * wps, "frac": A * wps / peaks["lop3"]},
             "fma_pipe": {"imad_per_s": F * wps, "frac": F * wps / peaks["imad"]}}
 
