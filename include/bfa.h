@@ -93,8 +93,9 @@ void bfa_free(bfa_prog* p);                                 /* NULL-safe */
 int bfa_info_get(const bfa_prog* p, bfa_info* out);
 
 /* Launch options (part of the JIT cache key).  Keys:
- *   "slot_bits"     log2 words per thread per iteration, 0..8   (default 2;
- *                   eval uses at most 5)
+ *   "slot_bits"     log2 words per thread per iteration, 0..14  (default 2;
+ *                   eval uses at most 5; each slot is a constant-folded
+ *                   cofactor in the body, so large values suit small programs)
  *   "thread_bits"   log2 threads per block, 5..10               (default 8)
  *   "inner_bits"    max log2 inner-loop trip count, 0..8        (default 4)
  *   "blocks_per_sm" resident blocks per SM targeted, 0 = occupancy API (default 0)

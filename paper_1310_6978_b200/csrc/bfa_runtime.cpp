@@ -2349,7 +2349,7 @@ int bfa_set_option(bfa_prog* p, const char* key, int64_t v) {
   p->graphs.clear();
   std::string k(key);
   auto bad = [&]() { return set_err(BFA_E_ARG, "option %s=%lld out of range", key, (long long)v); };
-  if (k == "slot_bits") { if (v < 0 || v > 8) return bad(); p->opt.slot_bits = (int)v; }
+  if (k == "slot_bits") { if (v < 0 || v > 14) return bad(); p->opt.slot_bits = (int)v; }
   else if (k == "thread_bits") { if (v < 5 || v > 10) return bad(); p->opt.thread_bits = (int)v; }
   else if (k == "inner_bits") { if (v < 0 || v > 8) return bad(); p->opt.inner_bits = (int)v; }
   else if (k == "blocks_per_sm") { if (v < 0 || v > 32) return bad(); p->opt.blocks_per_sm = (int)v; }

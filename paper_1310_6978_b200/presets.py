@@ -14,7 +14,11 @@ decided at preparation time.  Chosen by full-cube sweeps on a B200
              -> 144.5 ms per 2^42 (budget 400: 149 ms; one seed: spills, 223 ms;
              slot 6 / inner 3: 170 ms; slot 5 / inner 4 / budget 200: 229 ms;
              slot 8: 292-509 ms, i-cache and spills)
-  C4 (n=36): slot 8, inner 2 -> 0.079 ms per 2^36 (slot 5 / inner 4: 0.296 ms)
+  C4 (n=36): slot 14, thread 7, no inner loop -> 0.021 ms per 2^36 (slot 12:
+             0.030, slot 10: 0.040, slot 8 / inner 2: 0.068, slot 5 / inner 4:
+             0.296 ms; profiles/r02/sweep_c4_slots.jsonl).  A small program
+             (posets) folds most of its 2^14 slot cofactors to constants, so
+             the body stays short (0.04 cells per word) and preparation is 3.4 s
 
 cold(cfg): the plan of least preparation + ONE count (what a single cold
 bfa_count should run; bench.py's e2e): slot 5, inner 4, role budget 200 on
@@ -35,13 +39,14 @@ EXHAUSTIVE = {"slot_bits": 7, "thread_bits": 8, "inner_bits": 2, "dual_pipe": 1,
               "min_blocks": 0, "role_budget": 800, "role_seeds": 3, "kernel_cofactor_bits": 0, "split_pieces": 0}
 
 _EXHAUSTIVE_BY_CONFIG = {
-    "c4": dict(EXHAUSTIVE, slot_bits=8, inner_bits=2, role_budget=200, role_seeds=1),
+    "c4": dict(EXHAUSTIVE, slot_bits=14, thread_bits=7, inner_bits=0, role_budget=200, role_seeds=1),
 }
 
 COLD = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200, role_seeds=1)
 
 _COLD_BY_CONFIG = {
-    "c4": _EXHAUSTIVE_BY_CONFIG["c4"],
+    # slot 8: 0.13 s of preparation + 0.07 ms (the slot-14 kernel prepares in 3.4 s)
+    "c4": dict(EXHAUSTIVE, slot_bits=8, inner_bits=2, role_budget=200, role_seeds=1),
 }
 
 DECOMPOSED = dict(EXHAUSTIVE, slot_bits=5, inner_bits=4, role_budget=200, role_seeds=1, split_pieces=16384,

@@ -139,7 +139,7 @@ def test_generated_kernels_compile_sm100a(tmp_path):
 def test_options_validation():
     p = bfa.Program("x0")
     with pytest.raises(bfa.BfaError):
-        p.set_option("slot_bits", 9)
+        p.set_option("slot_bits", 15)
     with pytest.raises(bfa.BfaError):
         p.set_option("nonsense", 1)
     p.set_option("thread_bits", 7).set_option("inner_bits", 2)
@@ -256,7 +256,7 @@ def test_last_error_code():
         bfa.Program("x0 &")
     assert e.value.code == bfa.BFA_E_PARSE == bfa._load().bfa_last_error_code()
     with pytest.raises(bfa.BfaError):
-        bfa.Program("x0").set_option("slot_bits", 9)
+        bfa.Program("x0").set_option("slot_bits", 15)
     assert bfa._load().bfa_last_error_code() == bfa.BFA_E_ARG
 
 

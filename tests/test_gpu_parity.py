@@ -214,7 +214,8 @@ def test_exhaustive_bench_kernel_vs_oracle(cfg, plan):
     """The headline kernel bench.py times (presets.exhaustive(cfg) over the whole
     2^n cube: same variant, same searched roles, same cubin) against the
     oracle on 4 random sub-ranges of its enumeration order, 2^24 valuations
-    each (P-13; C5 cannot be oracle-checked whole).  bfa_count_positions runs
+    each for C5, 2^26 (one outer-iteration unit) for C4 (P-13; C5 cannot be
+    oracle-checked whole).  bfa_count_positions runs
     exactly that kernel; the oracle counts the renamed program f' on the same
     position range."""
     text, n, expect = W.config(cfg)
@@ -224,13 +225,14 @@ def test_exhaustive_bench_kernel_vs_oracle(cfg, plan):
     assert sorted(perm) == list(range(64)) and perm != list(range(64))
     text2 = renamed(text, perm)
     rng = np.random.default_rng(13106978)
+    span = 1 << (26 if cfg == "c4" else 24)   # >= one outer-iteration unit of the kernel
     for _ in range(4):
         if cfg == "c4":          # sub-ranges where every reflexivity letter is 1 (else no models)
-            lo = (int(rng.integers(0, 1 << 36)) | sum(1 << perm[35 - 7 * i] for i in range(6))) & ~((1 << 24) - 1)
+            lo = (int(rng.integers(0, 1 << 36)) | sum(1 << perm[35 - 7 * i] for i in range(6))) & ~(span - 1)
         else:
             lo = int(rng.integers(0, 1 << (n - 24))) << 24
-        got = int(p.count_positions(n, n, lo, lo + (1 << 24)).item())
-        assert got == oracle.count(text2, n, lo, lo + (1 << 24)), (cfg, lo)
+        got = int(p.count_positions(n, n, lo, lo + span).item())
+        assert got == oracle.count(text2, n, lo, lo + span), (cfg, lo)
     # the same compiled kernel over the whole cube: the count bench.py reports
     c = p.count(n)
     ll = bfa.last_launch()
